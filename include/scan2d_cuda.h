@@ -1,0 +1,148 @@
+/*
+ * scan2d_cuda.h -- C ABI of the B200 (sm_100a) 2D selective-scan library
+ *                  (libscan2d_cuda.so).
+ *
+ * Drop-in boundary for the hot path of the 2DMamba reference artifact
+ * (arXiv 2412.00678, /root/reference/proj):
+ *
+ *   scan2d_forward   replaces  scan2d::tiled_scan_2d_forward<T>
+ *                              (proj/include/scan2d/engine.hpp:88-94,
+ *                               proj/src/engine.cpp:154-243)
+ *   scan2d_backward  replaces  scan2d::tiled_scan_2d_backward<T>
+ *                              (proj/include/scan2d/engine.hpp:100-102,
+ *                               proj/src/engine.cpp:245-410)
+ *
+ * The reference's C++ template API itself is re-provided on top of this ABI by
+ * paper_2412_00678_b200/csrc/shim/engine_shim.cpp (libscan2d_engine_cuda.so).
+ *
+ * Conventions
+ *  - Plain C: no exceptions, no STL, no torch types.  Every pointer argument is
+ *    a DEVICE pointer unless stated; the caller owns every buffer, including the
+ *    workspace and the residual ("saved forward") buffer.
+ *  - Stream ordered: work is enqueued on `stream`; nothing synchronises the host.
+ *  - Deterministic: identical inputs give identical output bits run to run (no
+ *    floating-point atomics; scalar reductions use a fixed order).
+ *  - Thread safe across distinct (stream, workspace) pairs.
+ *
+ * Layouts (S scans = flattened batch x channel, per-scan reference Grid layout,
+ * types.hpp:55-57, N fastest):
+ *   x, z, y, dy, dx, dz          [S][H][W]
+ *   B, C, dB, dC                 [S/G][H][W][N]   (scan s uses B/C block s / G)
+ *   A, dA                        [P][N]           (scan s uses parameter row s % P)
+ *   Dskip, bias, dDskip, dbias   [P]
+ *   ph, pv (optional)            [S][kh][kw][T][N], kh = ceil(H/T), kw = ceil(W/T):
+ *                                the reference CarryState (engine.hpp:29-46)
+ * G = 1 and P = S is the reference operator contract (one scan per call);
+ * G = P = D channels is the 2DMamba block layout (model.cpp:150-193).
+ */
+#ifndef SCAN2D_CUDA_H
+#define SCAN2D_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (the reference throws std::invalid_argument / std::logic_error,
+ * engine.cpp:19-30, :163-164, :248-252; the C++ shim maps these back) */
+#define SCAN2D_OK 0
+#define SCAN2D_EINVAL 1        /* shape / argument error  (std::invalid_argument) */
+#define SCAN2D_ESTALE 2        /* no valid saved forward  (std::logic_error)      */
+#define SCAN2D_ECUDA 3         /* CUDA launch / runtime error                     */
+#define SCAN2D_ENOMEM 4        /* workspace too small                             */
+#define SCAN2D_EUNSUPPORTED 5  /* device is not sm_100                            */
+
+#define SCAN2D_F32 0
+#define SCAN2D_F64 1
+
+#define SCAN2D_OP_FWD 0
+#define SCAN2D_OP_BWD 1
+
+#define SCAN2D_MAX_STATE_DIM 2048 /* engine.cpp:19 kMaxStateDim */
+
+/* Opaque stream handle; binary compatible with cudaStream_t (CUstream_st*). */
+typedef struct CUstream_st* scan2d_stream_t;
+
+typedef struct scan2d_desc {
+  int64_t num_scans;    /* S >= 1                                              */
+  int32_t height;       /* H >= 1                                              */
+  int32_t width;        /* W >= 1                                              */
+  int32_t state_dim;    /* N in [1, 2048]                                      */
+  int32_t tile;         /* reference TileConfig T >= 1 (layout of ph / pv)     */
+  int32_t params_period;/* P >= 1, divides S                                    */
+  int32_t bc_group;     /* G >= 1, divides S                                    */
+  int32_t dtype;        /* SCAN2D_F32 or SCAN2D_F64                            */
+  int32_t reserved;     /* must be 0                                           */
+} scan2d_desc;
+
+/* Validates a descriptor (the checks of require_shapes, engine.cpp:21-30). */
+int scan2d_check_desc(const scan2d_desc* desc);
+
+/* Bytes of caller-provided scratch for one call of `op` (SCAN2D_OP_FWD/BWD). */
+size_t scan2d_workspace_bytes(const scan2d_desc* desc, int op);
+
+/* Bytes of the residual buffer a training forward fills and the backward reads:
+ * vertical-state checkpoints every few rows plus the horizontal carries at the
+ * kernel's column-group boundaries (the analogue of SavedForward's CarryState,
+ * engine.hpp:51-59).  Inputs are NOT copied: the backward takes them again. */
+size_t scan2d_residual_bytes(const scan2d_desc* desc);
+
+/* Forward: y = C.h + Dskip.x with h the 2D scan of (Abar = exp(delta A),
+ * Bbar x = delta B x), delta = softplus(z + bias).
+ *   y         required
+ *   ph, pv    optional (NULL): reference CarryState per scan for desc->tile
+ *   residual  optional (NULL = inference, reference save_residuals = false)
+ */
+int scan2d_forward(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                   const void* C, const void* A, const void* Dskip, const void* bias, void* y,
+                   void* ph, void* pv, void* residual, void* workspace, size_t workspace_bytes,
+                   scan2d_stream_t stream);
+
+/* Backward from the residual of a training forward with the same descriptor and
+ * inputs.  residual == NULL returns SCAN2D_ESTALE.  All gradient outputs are
+ * overwritten (not accumulated). */
+int scan2d_backward(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                    const void* C, const void* A, const void* Dskip, const void* bias,
+                    const void* residual, const void* dy, void* dx, void* dz, void* dA,
+                    void* dB, void* dC, void* dDskip, void* dbias, void* workspace,
+                    size_t workspace_bytes, scan2d_stream_t stream);
+
+/* Typed conveniences (desc->dtype is overridden). */
+int scan2d_fwd_f32(const scan2d_desc* desc, const float* x, const float* z, const float* B,
+                   const float* C, const float* A, const float* Dskip, const float* bias,
+                   float* y, float* ph, float* pv, void* residual, void* workspace,
+                   size_t workspace_bytes, scan2d_stream_t stream);
+int scan2d_fwd_f64(const scan2d_desc* desc, const double* x, const double* z, const double* B,
+                   const double* C, const double* A, const double* Dskip, const double* bias,
+                   double* y, double* ph, double* pv, void* residual, void* workspace,
+                   size_t workspace_bytes, scan2d_stream_t stream);
+int scan2d_bwd_f32(const scan2d_desc* desc, const float* x, const float* z, const float* B,
+                   const float* C, const float* A, const float* Dskip, const float* bias,
+                   const void* residual, const float* dy, float* dx, float* dz, float* dA,
+                   float* dB, float* dC, float* dDskip, float* dbias, void* workspace,
+                   size_t workspace_bytes, scan2d_stream_t stream);
+int scan2d_bwd_f64(const scan2d_desc* desc, const double* x, const double* z, const double* B,
+                   const double* C, const double* A, const double* Dskip, const double* bias,
+                   const void* residual, const double* dy, double* dx, double* dz, double* dA,
+                   double* dB, double* dC, double* dDskip, double* dbias, void* workspace,
+                   size_t workspace_bytes, scan2d_stream_t stream);
+
+/* Launch geometry the library picks for a descriptor (diagnostics / bench):
+ * out[0..7] = {lanes_per_chunk, cols_per_chunk, scans_per_warp, warps_per_scan,
+ *              warps_per_cta, ctas_per_scan_row, total_ctas, band_rows}. */
+int scan2d_plan_info(const scan2d_desc* desc, int op, int64_t* out8);
+
+/* Number of kernel launches the last scan2d_forward / scan2d_backward call on
+ * this host thread enqueued (memsets excluded). */
+int scan2d_last_launch_count(void);
+
+const char* scan2d_status_string(int status);
+int scan2d_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCAN2D_CUDA_H */

@@ -1,0 +1,114 @@
+"""ctypes binding of the C ABI (include/scan2d_cuda.h) -> lib/libscan2d_cuda.so.
+
+The library is built in-tree (``make -C paper_2412_00678_b200/csrc``, or
+``__graft_entry__.build()``).  There is no CPU fallback: if the shared object is
+missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libscan2d_cuda.so")
+
+OK, EINVAL, ESTALE, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4, 5
+F32, F64 = 0, 1
+OP_FWD, OP_BWD = 0, 1
+MAX_STATE_DIM = 2048
+
+# every symbol include/scan2d_cuda.h declares
+EXPORTED_SYMBOLS = (
+    "scan2d_check_desc",
+    "scan2d_workspace_bytes",
+    "scan2d_residual_bytes",
+    "scan2d_forward",
+    "scan2d_backward",
+    "scan2d_fwd_f32",
+    "scan2d_fwd_f64",
+    "scan2d_bwd_f32",
+    "scan2d_bwd_f64",
+    "scan2d_plan_info",
+    "scan2d_last_launch_count",
+    "scan2d_status_string",
+    "scan2d_version",
+)
+
+
+class Scan2dDesc(C.Structure):
+    """Mirror of ``scan2d_desc`` (include/scan2d_cuda.h)."""
+
+    _fields_ = [
+        ("num_scans", C.c_int64),
+        ("height", C.c_int32),
+        ("width", C.c_int32),
+        ("state_dim", C.c_int32),
+        ("tile", C.c_int32),
+        ("params_period", C.c_int32),
+        ("bc_group", C.c_int32),
+        ("dtype", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class Scan2dError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {status_string(status)} (status {status})")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA library must be built "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    D = C.POINTER(Scan2dDesc)
+    lib.scan2d_check_desc.argtypes = [D]
+    lib.scan2d_check_desc.restype = C.c_int
+    lib.scan2d_workspace_bytes.argtypes = [D, C.c_int]
+    lib.scan2d_workspace_bytes.restype = C.c_size_t
+    lib.scan2d_residual_bytes.argtypes = [D]
+    lib.scan2d_residual_bytes.restype = C.c_size_t
+    lib.scan2d_forward.argtypes = [D] + [P] * 11 + [C.c_size_t, P]
+    lib.scan2d_forward.restype = C.c_int
+    lib.scan2d_backward.argtypes = [D] + [P] * 17 + [C.c_size_t, P]
+    lib.scan2d_backward.restype = C.c_int
+    for name, n_in in (("scan2d_fwd_f32", 11), ("scan2d_fwd_f64", 11)):
+        getattr(lib, name).argtypes = [D] + [P] * n_in + [C.c_size_t, P]
+        getattr(lib, name).restype = C.c_int
+    for name in ("scan2d_bwd_f32", "scan2d_bwd_f64"):
+        getattr(lib, name).argtypes = [D] + [P] * 17 + [C.c_size_t, P]
+        getattr(lib, name).restype = C.c_int
+    lib.scan2d_plan_info.argtypes = [D, C.c_int, C.POINTER(C.c_int64)]
+    lib.scan2d_plan_info.restype = C.c_int
+    lib.scan2d_last_launch_count.argtypes = []
+    lib.scan2d_last_launch_count.restype = C.c_int
+    lib.scan2d_status_string.argtypes = [C.c_int]
+    lib.scan2d_status_string.restype = C.c_char_p
+    lib.scan2d_version.argtypes = []
+    lib.scan2d_version.restype = C.c_int
+    return lib
+
+
+lib = _load()
+
+
+def status_string(status: int) -> str:
+    return lib.scan2d_status_string(status).decode()
+
+
+def make_desc(S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=F32) -> Scan2dDesc:
+    return Scan2dDesc(int(S), int(H), int(W), int(N), int(tile),
+                      int(S if params_period is None else params_period), int(bc_group), int(dtype), 0)
+
+
+def plan_info(desc: Scan2dDesc, op: int = OP_FWD) -> dict:
+    out = (C.c_int64 * 8)()
+    rc = lib.scan2d_plan_info(C.byref(desc), op, out)
+    if rc != OK:
+        raise Scan2dError(rc, "scan2d_plan_info")
+    keys = ("lanes_per_chunk", "cols_per_chunk", "scans_per_warp", "warps_per_scan",
+            "warps_per_cta", "ctas_per_scan_row", "total_ctas", "band_rows")
+    return dict(zip(keys, [int(v) for v in out]))

@@ -1,0 +1,260 @@
+"""Host-side mirror of the reference scan API over the CUDA C ABI.
+
+Mirrors ``scan2d::tiled_scan_2d_forward`` / ``tiled_scan_2d_backward``
+(proj/include/scan2d/engine.hpp:82-102) with the same argument meaning and
+error behaviour, batched over S independent scans:
+
+=====================  =========================  ==================================
+reference              here                       notes
+=====================  =========================  ==================================
+``Grid<T> x`` [H,W]    ``x`` [S,H,W]               S = batch x channel (model.cpp:177)
+``inputs.z_raw``       ``z`` [S,H,W]
+``inputs.b / .c``      ``B, C`` [S/G,H,W,N]        G = bc_group (1 = reference contract)
+``params.a``           ``A`` [P,N]                 scan s uses row s % P
+``params.d_skip/bias`` ``Dskip, bias`` [P]
+``TileConfig``         ``tile``                    only shapes the optional carries
+``threads``            ``threads``                 accepted, no effect (already deterministic)
+``save_residuals``     ``save_residuals``          False -> saved.valid is False
+``CarryState``         ``carries=True``            ph, pv [S,kh,kw,T,N]
+=====================  =========================  ==================================
+
+Errors: shape problems raise ``ValueError`` (std::invalid_argument,
+engine.cpp:19-30, :163-164, :251-252); backward from an invalid saved state
+raises ``RuntimeError`` (std::logic_error, engine.cpp:248-249).
+
+All compute runs in libscan2d_cuda.so; torch is used for device memory and
+the current CUDA stream only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from . import _native as nat
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return nat.F32
+    if t.dtype == torch.float64:
+        return nat.F64
+    raise ValueError(f"scan2d: dtype {t.dtype} unsupported (float32 / float64 only)")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(device: torch.device):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check(cond: bool, msg: str):
+    if not cond:
+        raise ValueError(msg)
+
+
+@dataclass
+class SavedForward:
+    """Analogue of ``SavedForward<T>`` (engine.hpp:51-59).  Inputs are
+    referenced, not deep-copied (autograd convention: do not modify them in
+    place between forward and backward); ``residual`` holds the recompute
+    checkpoints and boundary carries."""
+
+    x: Optional[torch.Tensor] = None
+    z: Optional[torch.Tensor] = None
+    B: Optional[torch.Tensor] = None
+    C: Optional[torch.Tensor] = None
+    A: Optional[torch.Tensor] = None
+    Dskip: Optional[torch.Tensor] = None
+    bias: Optional[torch.Tensor] = None
+    residual: Optional[torch.Tensor] = None
+    desc: Optional[nat.Scan2dDesc] = None
+    valid: bool = False
+
+
+@dataclass
+class TiledForwardResult:
+    y: torch.Tensor
+    saved: SavedForward = field(default_factory=SavedForward)
+    ph: Optional[torch.Tensor] = None
+    pv: Optional[torch.Tensor] = None
+
+
+@dataclass
+class GradBundle:
+    """Analogue of ``GradBundle<T>`` (engine.hpp:71-80)."""
+
+    dx: torch.Tensor
+    dz_raw: torch.Tensor
+    da: torch.Tensor
+    db: torch.Tensor
+    dc: torch.Tensor
+    dd: torch.Tensor
+    dbias: torch.Tensor
+
+
+def _normalise(x, z, B, C_, A, Dskip, bias):
+    """Accept single-scan reference shapes ([H,W], [H,W,N], [N], scalar) or batched ones."""
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    if z.dim() == 2:
+        z = z.unsqueeze(0)
+    if B.dim() == 3:
+        B = B.unsqueeze(0)
+    if C_.dim() == 3:
+        C_ = C_.unsqueeze(0)
+    if A.dim() == 1:
+        A = A.unsqueeze(0)
+    Dskip = Dskip.reshape(-1)
+    bias = bias.reshape(-1)
+    return x, z, B, C_, A, Dskip, bias
+
+
+def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int) -> nat.Scan2dDesc:
+    """require_shapes (engine.cpp:21-30) + TileConfig (types.hpp:133-146) checks."""
+    _check(x.dim() == 3, "scan input must be [S,H,W] (single channel per scan)")
+    S, H, W = x.shape
+    _check(tuple(z.shape) == (S, H, W), "input and selective grids must share H and W")
+    _check(B.dim() == 4 and C_.dim() == 4, "B and C must be [S/G,H,W,N]")
+    _check(tuple(B.shape[1:3]) == (H, W) and tuple(C_.shape[1:3]) == (H, W),
+           "input and selective grids must share H and W")
+    _check(B.shape == C_.shape, "SelectiveInputs: B and C must share N")
+    N = B.shape[3]
+    _check(A.dim() == 2 and A.shape[1] == N, "state dimension mismatch between inputs and params")
+    _check(N <= nat.MAX_STATE_DIM, "state dimension too large")
+    P = A.shape[0]
+    _check(Dskip.numel() == P and bias.numel() == P, "Dskip / bias must have one entry per A row")
+    _check(S % P == 0, "number of scans must be a multiple of the parameter rows")
+    _check(B.shape[0] >= 1 and S % B.shape[0] == 0, "number of scans must be a multiple of B/C blocks")
+    _check(tile > 0, "TileConfig: T must be positive")
+    for t in (x, z, B, C_, A, Dskip, bias):
+        _check(t.is_cuda, "scan2d: tensors must be CUDA tensors (no CPU fallback)")
+        _check(t.dtype == x.dtype, "scan2d: all tensors must share one dtype")
+        _check(t.device == x.device, "scan2d: all tensors must be on one device")
+    G = S // B.shape[0]
+    desc = nat.make_desc(S, H, W, N, tile=tile, params_period=P, bc_group=G, dtype=_dtype_code(x))
+    rc = nat.lib.scan2d_check_desc(C.byref(desc))
+    if rc == nat.EINVAL:
+        raise ValueError(nat.status_string(rc))
+    if rc != nat.OK:
+        raise nat.Scan2dError(rc, "scan2d_check_desc")
+    return desc
+
+
+def tiled_scan_2d_forward(x, z, B, C_, A, Dskip, bias, tile: int = 16, threads: int = 1,
+                          save_residuals: bool = True, carries: bool = False,
+                          counter=None) -> TiledForwardResult:
+    """Batched ``tiled_scan_2d_forward`` (engine.hpp:88-94) on the GPU.
+
+    ``counter`` (a dict) is filled with the reference element-transfer model
+    (engine.cpp:222-229 == memsim.cpp:38-71) when given."""
+    del threads  # results are thread-invariant by construction
+    x, z, B, C_, A, Dskip, bias = _normalise(x, z, B, C_, A, Dskip, bias)
+    x, z, B, C_, A, Dskip, bias = [t.contiguous() for t in (x, z, B, C_, A, Dskip, bias)]
+    desc = make_desc_for(x, z, B, C_, A, Dskip, bias, tile)
+    S, H, W = x.shape
+    N = B.shape[3]
+    dev = x.device
+    y = torch.empty((S, H, W), dtype=x.dtype, device=dev)
+    ph = pv = None
+    if carries:
+        kh, kw = -(-H // tile), -(-W // tile)
+        ph = torch.empty((S, kh, kw, tile, N), dtype=x.dtype, device=dev)
+        pv = torch.empty_like(ph)
+    residual = None
+    if save_residuals:
+        residual = torch.empty(nat.lib.scan2d_residual_bytes(C.byref(desc)), dtype=torch.uint8, device=dev)
+    wsb = nat.lib.scan2d_workspace_bytes(C.byref(desc), nat.OP_FWD)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        rc = nat.lib.scan2d_forward(C.byref(desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A), _ptr(Dskip),
+                                    _ptr(bias), _ptr(y), _ptr(ph), _ptr(pv), _ptr(residual), _ptr(ws), wsb,
+                                    _stream(dev))
+    if rc == nat.EINVAL:
+        raise ValueError(nat.status_string(rc))
+    if rc != nat.OK:
+        raise nat.Scan2dError(rc, "scan2d_forward")
+    if counter is not None:
+        _charge_counter(counter, S, H, W, N, tile)
+    saved = SavedForward()
+    if save_residuals:
+        saved = SavedForward(x, z, B, C_, A, Dskip, bias, residual, desc, True)
+    return TiledForwardResult(y=y, saved=saved, ph=ph, pv=pv)
+
+
+def tiled_scan_2d_backward(saved: SavedForward, dy: torch.Tensor, threads: int = 1) -> GradBundle:
+    """Batched ``tiled_scan_2d_backward`` (engine.hpp:100-102) on the GPU."""
+    del threads
+    if saved is None or not saved.valid:
+        raise RuntimeError("tiled_scan_2d_backward: stale saved forward state")
+    x = saved.x
+    if dy.dim() == 2:
+        dy = dy.unsqueeze(0)
+    if tuple(dy.shape) != tuple(x.shape):
+        raise ValueError("tiled_scan_2d_backward: dy shape mismatch")
+    dy = dy.contiguous()
+    _check(dy.dtype == x.dtype and dy.device == x.device, "dy must match the forward's dtype/device")
+    desc = saved.desc
+    S, H, W = x.shape
+    N = saved.B.shape[3]
+    P = saved.A.shape[0]
+    dev = x.device
+    dx = torch.empty_like(x)
+    dz = torch.empty_like(x)
+    dB = torch.empty_like(saved.B)
+    dC = torch.empty_like(saved.C)
+    dA = torch.empty((P, N), dtype=x.dtype, device=dev)
+    dD = torch.empty((P,), dtype=x.dtype, device=dev)
+    dbias = torch.empty((P,), dtype=x.dtype, device=dev)
+    wsb = nat.lib.scan2d_workspace_bytes(C.byref(desc), nat.OP_BWD)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        rc = nat.lib.scan2d_backward(C.byref(desc), _ptr(x), _ptr(saved.z), _ptr(saved.B), _ptr(saved.C),
+                                     _ptr(saved.A), _ptr(saved.Dskip), _ptr(saved.bias), _ptr(saved.residual),
+                                     _ptr(dy), _ptr(dx), _ptr(dz), _ptr(dA), _ptr(dB), _ptr(dC), _ptr(dD),
+                                     _ptr(dbias), _ptr(ws), wsb, _stream(dev))
+    if rc == nat.ESTALE:
+        raise RuntimeError("tiled_scan_2d_backward: " + nat.status_string(rc))
+    if rc == nat.EINVAL:
+        raise ValueError(nat.status_string(rc))
+    if rc != nat.OK:
+        raise nat.Scan2dError(rc, "scan2d_backward")
+    return GradBundle(dx=dx, dz_raw=dz, da=dA, db=dB, dc=dC, dd=dD, dbias=dbias)
+
+
+def _charge_counter(counter: dict, S, H, W, N, t):
+    """Reference counting model per tile (engine.cpp:222-229), summed over S scans."""
+    kh, kw = -(-H // t), -(-W // t)
+    flat = -(-(t * t) // 32) * 32
+    cells = H * W
+    add = dict(payload_reads=S * (2 * cells + 2 * cells * N), payload_writes=S * cells,
+               intermediate_traffic=0, carry_traffic=S * kh * kw * 4 * t * N,
+               padding_elements=S * 2 * N * (kh * kw * flat - cells))
+    for k, v in add.items():
+        counter[k] = counter.get(k, 0) + v
+
+
+class Scan2dFunction(torch.autograd.Function):
+    """Autograd binding: y = scan2d(x, z, B, C, A, Dskip, bias)."""
+
+    @staticmethod
+    def forward(ctx, x, z, B, C_, A, Dskip, bias, tile: int = 16):
+        res = tiled_scan_2d_forward(x, z, B, C_, A, Dskip, bias, tile=tile, save_residuals=True)
+        ctx.saved_fwd = res.saved
+        ctx.shapes = (x.shape, z.shape, B.shape, C_.shape, A.shape, Dskip.shape, bias.shape)
+        return res.y.reshape(x.shape)
+
+    @staticmethod
+    def backward(ctx, dy):
+        g = tiled_scan_2d_backward(ctx.saved_fwd, dy.reshape(ctx.saved_fwd.x.shape))
+        shapes = ctx.shapes
+        outs = (g.dx, g.dz_raw, g.db, g.dc, g.da, g.dd, g.dbias)
+        return tuple(o.reshape(s) for o, s in zip(outs, shapes)) + (None,)
+
+
+def scan2d(x, z, B, C_, A, Dskip, bias, tile: int = 16):
+    return Scan2dFunction.apply(x, z, B, C_, A, Dskip, bias, tile)
