@@ -71,11 +71,11 @@ def _load():
     lib.scan2d_workspace_bytes.restype = C.c_size_t
     lib.scan2d_residual_bytes.argtypes = [D]
     lib.scan2d_residual_bytes.restype = C.c_size_t
-    lib.scan2d_forward.argtypes = [D] + [P] * 11 + [C.c_size_t, P]
+    lib.scan2d_forward.argtypes = [D] + [P] * 12 + [C.c_size_t, P]
     lib.scan2d_forward.restype = C.c_int
     lib.scan2d_backward.argtypes = [D] + [P] * 17 + [C.c_size_t, P]
     lib.scan2d_backward.restype = C.c_int
-    for name, n_in in (("scan2d_fwd_f32", 11), ("scan2d_fwd_f64", 11)):
+    for name, n_in in (("scan2d_fwd_f32", 12), ("scan2d_fwd_f64", 12)):
         getattr(lib, name).argtypes = [D] + [P] * n_in + [C.c_size_t, P]
         getattr(lib, name).restype = C.c_int
     for name in ("scan2d_bwd_f32", "scan2d_bwd_f64"):
