@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 2D selective scan (fwd + bwd) vs the CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+
+One "step" = one training pass of the hot path over one batch: scan2d_forward
+(saving the residual) followed by scan2d_backward, on synthetic inputs
+resident in HBM (the `value`).  `e2e` repeats the step through the same C ABI
+from pinned HOST buffers with every input copied in and every output
+(y and all gradients) copied back inside the timed region -- the drop-in
+replacement of the reference call, whose arguments and results live on the host.
+
+Workloads (BASELINE.json configs):
+  cfg1  S=64   16x16   N=16 fwd           (configs[0], the CPU-oracle case)
+  cfg2  S=128  200x200 N=16 fwd+bwd       (configs[1], DEFAULT: WSI MIL scale)
+  cfg3  S=12288 56x56  N=1  fwd+bwd       (configs[2], VMamba stage 1, B=64 D=192)
+  cfg4a..d  B=64 N=1 fwd+bwd: 56x56 D=96, 28x28 D=192, 14x14 D=384, 7x7 D=768
+  cfg5  S=256  1024x1024 N=16 fwd         (configs[4], giga-pixel slide)
+
+Multi-GPU (torchrun, one rank per GPU): every rank processes its own S scans
+(weak scaling, no collective on the data path); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
+
+METRIC = "2D sel-scan Gelem/s & HBM GB/s (% roofline) at 1/2/4/8 B200 vs CPU ref"
+
+WORKLOADS = {
+    "cfg1": dict(S=64, H=16, W=16, N=16, bwd=False, desc="B=1 D=64 N=16 16x16 fwd (configs[0])"),
+    "cfg2": dict(S=128, H=200, W=200, N=16, bwd=True, desc="WSI MIL: B=1 D=128 N=16 200x200 fwd+bwd (configs[1])"),
+    "cfg3": dict(S=64 * 192, H=56, W=56, N=1, bwd=True, desc="VMamba stage-1: B=64 D=192 N=1 56x56 fwd+bwd (configs[2])"),
+    "cfg4a": dict(S=64 * 96, H=56, W=56, N=1, bwd=True, desc="VMamba sweep: B=64 D=96 N=1 56x56 fwd+bwd (configs[3])"),
+    "cfg4b": dict(S=64 * 192, H=28, W=28, N=1, bwd=True, desc="VMamba sweep: B=64 D=192 N=1 28x28 fwd+bwd (configs[3])"),
+    "cfg4c": dict(S=64 * 384, H=14, W=14, N=1, bwd=True, desc="VMamba sweep: B=64 D=384 N=1 14x14 fwd+bwd (configs[3])"),
+    "cfg4d": dict(S=64 * 768, H=7, W=7, N=1, bwd=True, desc="VMamba sweep: B=64 D=768 N=1 7x7 fwd+bwd (configs[3])"),
+    "cfg5": dict(S=256, H=1024, W=1024, N=16, bwd=False, desc="giga-pixel: B=1 D=256 N=16 1024x1024 fwd (configs[4])"),
+}
+
+L2_BYTES = 126 * 1024 * 1024
+NVML_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def alg_bytes(wl, es=4):
+    """Reference counting model (memsim.cpp:45-46): per scan
+    fwd = es*H*W*(3+2N) (x, z, B, C in; y out), bwd = es*H*W*(5+4N)
+    (x, z, dy, B, C in; dx, dz, dB, dC out)."""
+    hw = wl["H"] * wl["W"]
+    return wl["S"] * es * hw * (3 + 2 * wl["N"]), wl["S"] * es * hw * (5 + 4 * wl["N"])
+
+
+def measured_peak():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy_ burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload, {})
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """NVML clocks / throttle reasons sampled in a background thread."""
+
+    def __init__(self, index=0, period=0.01):
+        self.samples = []
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        if not self.ok:
+            return
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                clk = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), clk, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self, t0, t1):
+        win = [s for s in self.samples if t0 <= s[0] <= t1] or self.samples
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        bits = 0
+        for s in win:
+            bits |= s[2]
+        reasons = [v for k, v in NVML_REASONS.items() if bits & k and k != 0x1]
+        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(win)}
+
+
+# ----------------------------------------------------------------- inputs
+
+
+def synth_inputs(torch, wl, dev, seed, dtype):
+    """random_instance distribution (fixtures.hpp:20-37): x, z, B, C ~ N(0,1),
+    A ~ -U(0.05, 0.95), D ~ N(0,1), bias ~ U(-0.5, 0.5); dy ~ N(0,1)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    S, H, W, N = wl["S"], wl["H"], wl["W"], wl["N"]
+    r = lambda *s: torch.randn(*s, generator=g, device=dev, dtype=dtype)
+    u = lambda *s: torch.rand(*s, generator=g, device=dev, dtype=dtype)
+    x, z = r(S, H, W), r(S, H, W)
+    B, C = r(S, H, W, N), r(S, H, W, N)
+    A = -(0.05 + 0.9 * u(S, N))
+    D = r(S)
+    bias = u(S) - 0.5
+    dy = r(S, H, W)
+    return [x, z, B, C, A, D, bias], dy
+
+
+def host_inputs_np(wl, S_sample, seed=1234):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    H, W, N = wl["H"], wl["W"], wl["N"]
+    f = lambda *s: rng.standard_normal(s, dtype=np.float32)
+    x, z, B, C = f(S_sample, H, W), f(S_sample, H, W), f(S_sample, H, W, N), f(S_sample, H, W, N)
+    A = -(0.05 + 0.9 * rng.random((S_sample, N), dtype=np.float32))
+    D = f(S_sample)
+    bias = rng.random(S_sample, dtype=np.float32) - 0.5
+    dy = f(S_sample, H, W)
+    return x, z, B, C, A, D, bias, dy
+
+
+# ------------------------------------------------------------ CPU reference
+
+
+class CpuReference:
+    """Reference CPU engine (oracle/_ref/libscan2d_ref.so: the reference's own
+    tiled_scan_2d_forward/backward, threads=1 per scan, scans spread over all
+    host cores in contiguous blocks -- the model.cpp:177 pattern) on a bounded
+    sample of the workload.  Falls back to the oracle port (kind "port") when
+    the reference library was not built."""
+
+    def __init__(self, wl, target_s=10.0):
+        sys.path.insert(0, os.path.join(REPO, "tests"))
+        self.wl = wl
+        self.kind = "reference"
+        try:
+            from oracle_lib import RefLib
+
+            self.ref = RefLib()
+        except Exception:
+            from oracle_lib import Oracle
+
+            self.ref = None
+            self.orc = Oracle()
+            self.kind = "port"
+        cores = os.cpu_count() or 1
+        self.t1 = self._run(1, 1, host_inputs_np(wl, 1, seed=99))
+        threads = cores if (self.ref is not None or not wl["bwd"]) else 1
+        k = int(max(threads, min(wl["S"], target_s * threads / max(self.t1, 1e-6) / 4)))
+        self.k = min(k, wl["S"])
+        self.threads = min(threads, self.k)
+        self.arrs = host_inputs_np(wl, self.k, seed=7)
+
+    def _run(self, S_, threads, arrs):
+        wl = self.wl
+        H, W, N, bwd = wl["H"], wl["W"], wl["N"], wl["bwd"]
+        x, z, B, C, A, D, bias, dy = arrs
+        if self.ref is not None:
+            secs, _ = self.ref.batch(S_, S_, 1, H, W, N, 16, threads, bwd, x, z, B, C, A, D, bias, dy)
+            return secs
+        t0 = time.perf_counter()
+        self.orc.fwd_batch(S_, S_, 1, H, W, N, x, z, B, C, A, D, bias, dtype="f32", threads=threads)
+        if bwd:
+            self.orc.bwd_batch(S_, S_, 1, H, W, N, x, z, B, C, A, D, bias, dy, dtype="f32")
+        return time.perf_counter() - t0
+
+    def step(self):
+        """One timed pass over the sample; returns seconds."""
+        return self._run(self.k, self.threads, self.arrs)
+
+    def gelem_s(self, secs):
+        return self.k * self.wl["H"] * self.wl["W"] / secs / 1e9
+
+    def describe(self, secs, reps):
+        wl = self.wl
+        return {"value": self.gelem_s(secs), "unit": "Gelem/s", "cores": self.threads, "kind": self.kind,
+                "sample": (f"{self.k} of {wl['S']} scans ({'fwd+bwd' if wl['bwd'] else 'fwd'}, T=16, "
+                           f"tiled_scan_2d_* threads=1 per scan) over {self.threads} host threads, "
+                           f"best of {reps}; one scan single-threaded {self.t1 * 1e3:.2f} ms")}
+
+
+def cpu_reference(wl, target_s=10.0, reps=3):
+    cr = CpuReference(wl, target_s)
+    best = min(cr.step() for _ in range(reps))
+    return cr.describe(best, reps)
+
+
+# ----------------------------------------------------------------- main
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="f32", choices=["f32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": args.workload, "desc": wl["desc"], "S_per_gpu": wl["S"], "H": wl["H"], "W": wl["W"],
+              "N": wl["N"], "tile": 16, "pass": "fwd+bwd" if wl["bwd"] else "fwd",
+              "parallelism": f"scan-sharded x{world} (no collectives)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        cr = CpuReference(wl, target_s=2.0)
+        for _ in range(args.warmup):
+            cr.step()
+        times = [cr.step() for _ in range(args.steps)]
+        mean_s = statistics.mean(times)
+        value = cr.gelem_s(mean_s)
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+                "data": "synthetic (random_instance distribution)", "config": config,
+                "cpu_baseline": dict(cr.describe(mean_s, args.steps), value=value),
+                "e2e": {"value": value, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2412_00678_b200.api import Scan2dOp
+
+    dtype = torch.float32
+    ins, dy = synth_inputs(torch, wl, dev, 1234 + rank, dtype)
+    op = Scan2dOp(wl["S"], wl["H"], wl["W"], wl["N"], tile=16, dtype=dtype, device=dev, with_backward=wl["bwd"])
+
+    def step():
+        op.forward(*ins, save=wl["bwd"])
+        if wl["bwd"]:
+            op.backward(*ins, dy)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    op.launches = 0
+    torch.cuda.synchronize()
+    barrier()
+    t_host0 = time.perf_counter()
+    e_start.record(stream)
+    for k in range(args.steps):
+        e0, e1, e2 = evs[k]
+        e0.record(stream)
+        op.forward(*ins, save=wl["bwd"])
+        e1.record(stream)
+        if wl["bwd"]:
+            op.backward(*ins, dy)
+        e2.record(stream)
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    t_host1 = time.perf_counter()
+    barrier()
+    launches = op.launches
+    total_ms = e_start.elapsed_time(e_end)
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in evs)
+    bwd_ms = statistics.mean(b.elapsed_time(c) for _, b, c in evs) if wl["bwd"] else 0.0
+    if dist is not None:
+        t = torch.tensor([total_ms, fwd_ms, bwd_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, fwd_ms, bwd_ms = [float(v) for v in t.tolist()]
+    sampler.stop()
+    clocks = sampler.summary(t_host0, t_host1)
+    ms_per_step = total_ms / args.steps
+    elems = wl["S"] * wl["H"] * wl["W"] * world
+    value = elems / (ms_per_step * 1e-3) / 1e9
+
+    fb, bb = alg_bytes(wl)
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic(args.workload)
+    if wl["bwd"]:
+        dom_name, dom_bytes, dom_ms = "scan2d_bwd_kernel", bb, bwd_ms
+    else:
+        dom_name, dom_bytes, dom_ms = "scan2d_fwd_kernel", fb, fwd_ms
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_src,
+            "traffic": traffic.get(dom_name, {}).get("dram_bytes_per_launch"),
+            "algorithmic_bytes_per_launch": dom_bytes,
+            "launch_ms": dom_ms}
+    extra = {"fwd_ms": fwd_ms, "fwd_gbs": fb / (fwd_ms * 1e-3) / 1e9, "fwd_frac": fb / (fwd_ms * 1e-3) / 1e9 / peak}
+    if wl["bwd"]:
+        extra.update({"bwd_ms": bwd_ms, "bwd_gbs": bb / (bwd_ms * 1e-3) / 1e9,
+                      "bwd_frac": bb / (bwd_ms * 1e-3) / 1e9 / peak})
+    extra["plan"] = op.plan()
+    extra["inputs_vs_l2"] = f"inputs {fb / 1e6:.0f} MB {'>' if fb > L2_BYTES else '<='} L2 {L2_BYTES / 1e6:.0f} MB"
+
+    # ---- e2e through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hin = [t.cpu().pin_memory() for t in ins]
+        hdy = dy.cpu().pin_memory()
+        outs_dev = [op.y] + ([op.dx, op.dz, op.dA, op.dB, op.dC, op.dD, op.dbias] if wl["bwd"] else [])
+        hout = [torch.empty_like(t, device="cpu").pin_memory() for t in outs_dev]
+        dins = [torch.empty_like(t) for t in ins]
+        ddy = torch.empty_like(dy)
+        h2d = sum(t.numel() * t.element_size() for t in hin) + (hdy.numel() * 4 if wl["bwd"] else 0)
+        d2h = sum(t.numel() * t.element_size() for t in hout)
+
+        def e2e_step():
+            for d, h in zip(dins, hin):
+                d.copy_(h, non_blocking=True)
+            if wl["bwd"]:
+                ddy.copy_(hdy, non_blocking=True)
+            op.forward(*dins, save=wl["bwd"])
+            if wl["bwd"]:
+                op.backward(*dins, ddy)
+            for h, d in zip(hout, outs_dev):
+                h.copy_(d, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        e2e_step()
+        barrier()
+        k2 = max(1, args.e2e_steps)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ea.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e_ms = ea.elapsed_time(eb) / k2
+        if dist is not None:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": elems / (e_ms * 1e-3) / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": k2,
+               "path": "C ABI (scan2d_forward/backward) with pinned host buffers; inputs+dy H2D, y+all grads D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference(wl)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "Gelem/s", "cores": 0, "kind": "unavailable", "sample": str(exc)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (random_instance distribution, generated on device)",
+                "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks, **extra}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -238,6 +238,63 @@ def _charge_counter(counter: dict, S, H, W, N, t):
         counter[k] = counter.get(k, 0) + v
 
 
+class Scan2dOp:
+    """Preallocated forward+backward for a fixed descriptor: keeps the
+    workspaces, residual and output buffers across calls so a training loop
+    enqueues exactly the library's kernels (no allocator traffic)."""
+
+    def __init__(self, S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=torch.float32,
+                 device="cuda", with_backward=True):
+        self.dev = torch.device(device)
+        self.dtype = dtype
+        code = nat.F64 if dtype == torch.float64 else nat.F32
+        self.desc = nat.make_desc(S, H, W, N, tile=tile, params_period=params_period, bc_group=bc_group,
+                                  dtype=code)
+        rc = nat.lib.scan2d_check_desc(C.byref(self.desc))
+        if rc != nat.OK:
+            raise ValueError(nat.status_string(rc))
+        P = S if params_period is None else params_period
+        self.shape = (S, H, W, N, P, S // bc_group)
+        e = lambda *s: torch.empty(s, dtype=dtype, device=self.dev)
+        self.y = e(S, H, W)
+        self.wsf_bytes = nat.lib.scan2d_workspace_bytes(C.byref(self.desc), nat.OP_FWD)
+        self.wsf = torch.empty(max(self.wsf_bytes, 1), dtype=torch.uint8, device=self.dev)
+        self.residual = None
+        if with_backward:
+            self.residual = torch.empty(nat.lib.scan2d_residual_bytes(C.byref(self.desc)), dtype=torch.uint8,
+                                        device=self.dev)
+            self.wsb_bytes = nat.lib.scan2d_workspace_bytes(C.byref(self.desc), nat.OP_BWD)
+            self.wsb = torch.empty(max(self.wsb_bytes, 1), dtype=torch.uint8, device=self.dev)
+            G = S // bc_group
+            self.dx, self.dz = e(S, H, W), e(S, H, W)
+            self.dB, self.dC = e(G, H, W, N), e(G, H, W, N)
+            self.dA, self.dD, self.dbias = e(P, N), e(P), e(P)
+        self.launches = 0
+
+    def forward(self, x, z, B, C_, A, Dskip, bias, save=True):
+        rc = nat.lib.scan2d_forward(C.byref(self.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A), _ptr(Dskip),
+                                    _ptr(bias), _ptr(self.y), None, None,
+                                    _ptr(self.residual) if save else None, _ptr(self.wsf), self.wsf_bytes,
+                                    _stream(self.dev))
+        if rc != nat.OK:
+            raise nat.Scan2dError(rc, "scan2d_forward")
+        self.launches += nat.lib.scan2d_last_launch_count()
+        return self.y
+
+    def backward(self, x, z, B, C_, A, Dskip, bias, dy):
+        rc = nat.lib.scan2d_backward(C.byref(self.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
+                                     _ptr(Dskip), _ptr(bias), _ptr(self.residual), _ptr(dy), _ptr(self.dx),
+                                     _ptr(self.dz), _ptr(self.dA), _ptr(self.dB), _ptr(self.dC), _ptr(self.dD),
+                                     _ptr(self.dbias), _ptr(self.wsb), self.wsb_bytes, _stream(self.dev))
+        if rc != nat.OK:
+            raise nat.Scan2dError(rc, "scan2d_backward")
+        self.launches += nat.lib.scan2d_last_launch_count()
+        return self.dx, self.dz, self.dA, self.dB, self.dC, self.dD, self.dbias
+
+    def plan(self) -> dict:
+        return nat.plan_info(self.desc)
+
+
 class Scan2dFunction(torch.autograd.Function):
     """Autograd binding: y = scan2d(x, z, B, C, A, Dskip, bias)."""
 
