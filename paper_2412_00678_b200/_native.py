@@ -109,6 +109,6 @@ def plan_info(desc: Scan2dDesc, op: int = OP_FWD) -> dict:
     rc = lib.scan2d_plan_info(C.byref(desc), op, out)
     if rc != OK:
         raise Scan2dError(rc, "scan2d_plan_info")
-    keys = ("lanes_per_chunk", "cols_per_chunk", "scans_per_warp", "warps_per_scan",
-            "warps_per_cta", "ctas_per_scan_row", "total_ctas", "band_rows")
+    keys = ("spl_x100_plus_lpc", "cols_per_chunk", "scans_per_warp", "warps_per_scan",
+            "cols_per_warp", "smem_bytes", "warps_total", "band_rows")
     return dict(zip(keys, [int(v) for v in out]))

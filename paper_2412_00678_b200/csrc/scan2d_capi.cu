@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 
@@ -45,73 +46,98 @@ int check_desc(const scan2d_desc* d) {
   return SCAN2D_OK;
 }
 
-// Launch geometry.  One plan serves both directions: the backward consumes the
-// forward's residual, whose layout depends on (ncb, nw, colsw, K).
-Plan make_plan(const scan2d_desc& d) {
-  Plan p{};
-  const int N = d.state_dim, W = d.width, H = d.height;
+// Geometry of one direction (see s2d::Geo).  N <= 128: SPL = 4 states per lane
+// (float4), LPC = Np / 4 lanes per chunk; N <= 2 uses SPL = Np, LPC = 1.
+s2d::Geo make_geo(const scan2d_desc& d, bool bwd) {
+  s2d::Geo g{};
+  const int N = d.state_dim, W = d.width;
   const bool dbl = d.dtype == SCAN2D_F64;
-  p.lpc = std::min(32, next_pow2(N));
-  p.cpw = 32 / p.lpc;
-  // columns per lane: wide enough to amortise the per-row shuffle scan, small
-  // enough to keep the vertical state and the prefetched row in registers
-  if (p.lpc >= 4) {
-    p.J = 4;
+  const int Np = next_pow2(N);
+  g.spl = Np >= 4 ? 4 : Np;
+  g.lpc = Np / g.spl;
+  g.cpw = 32 / g.lpc;
+  if (g.spl == 4)
+    g.J = bwd ? 2 : 4;
+  else
+    g.J = bwd ? 4 : 8;
+  if (dbl) g.J = std::min(g.J, 2);
+  const int chunks = static_cast<int>(ceil_div(W, g.J));
+  if (chunks <= g.cpw / 2) {
+    g.cps = next_pow2(chunks);
+    g.seg = g.cpw / g.cps;
   } else {
-    const int need = static_cast<int>(ceil_div(W, p.cpw));
-    p.J = std::min(8, next_pow2(std::max(1, need)));
+    g.cps = g.cpw;
+    g.seg = 1;
   }
-  if (dbl) p.J = std::min(p.J, 4);
-  const int chunks_per_scan = static_cast<int>(ceil_div(W, p.J));
-  if (chunks_per_scan <= p.cpw / 2) {
-    // narrow grids: pack several scans into one warp (segmented shuffles)
-    p.cps = next_pow2(chunks_per_scan);
-    p.seg = p.cpw / p.cps;
-  } else {
-    p.cps = p.cpw;
-    p.seg = 1;
-  }
-  p.colsw = p.cps * p.J;
-  p.wreal = static_cast<int>(ceil_div(W, p.colsw));
-  if (p.seg > 1) p.wreal = 1;
-  if (p.wreal <= 16) {
-    p.ncb = 1;
-    p.wps = p.wreal;
-    p.nw = p.wps * std::max(1, 8 / p.wps);
-  } else {
-    p.ncb = static_cast<int>(ceil_div(p.wreal, 16));
-    p.nw = static_cast<int>(ceil_div(p.wreal, p.ncb));
-    p.wps = p.nw * p.ncb;
-  }
-  p.units = ceil_div(d.num_scans, p.seg) * p.wps;
-  p.ctas = ceil_div(p.units, p.nw);
-  p.K = std::min(8, H);
-  p.nb = static_cast<int>(ceil_div(H, p.K));
-  return p;
+  g.colsw = g.cps * g.J;
+  g.wreal = g.seg > 1 ? 1 : static_cast<int>(ceil_div(W, g.colsw));
+  g.units = ceil_div(d.num_scans, g.seg) * g.wreal;
+  g.stages = bwd ? 3 : 4;
+  return g;
 }
 
+int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K) {
+  const bool dbl = d.dtype == SCAN2D_F64;
+  g.stage_elems = dbl ? s2d::stage_elems<double>(g.colsw, d.state_dim, g.seg, bwd)
+                      : s2d::stage_elems<float>(g.colsw, d.state_dim, g.seg, bwd);
+  size_t elems = static_cast<size_t>(g.stages) * g.stage_elems;
+  if (bwd) elems += dbl ? s2d::band_elems<double>(K, g.J, g.spl) : s2d::band_elems<float>(K, g.J, g.spl);
+  const size_t bytes = elems * dtype_size(d.dtype);
+  if (bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
+  g.smem_bytes = static_cast<int>(bytes);
+  return SCAN2D_OK;
+}
+
+// One plan serves both directions: the backward consumes the forward's
+// residual (checkpoints every K rows, carries every Q columns).
+int make_plan(const scan2d_desc& d, Plan& p) {
+  p = Plan{};
+  p.b = make_geo(d, true);
+  p.f = make_geo(d, false);
+  p.K = std::min(8, static_cast<int>(d.height));
+  p.nb = static_cast<int>(ceil_div(d.height, p.K));
+  if (p.b.wreal > 1) {
+    p.Q = p.b.colsw;
+    p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
+    // forward warp boundaries and chunk starts must sit on the Q grid
+    const bool ok = (p.Q % p.f.J) == 0 && (p.f.wreal == 1 || (p.f.colsw % p.Q) == 0);
+    if (!ok) p.f = p.b, p.f.stages = 4;
+  } else {
+    p.Q = std::max(1, d.width);
+    p.nq = 0;
+  }
+  if (p.f.wreal > 1 && p.nq == 0) {  // forward chains need carry slots too
+    p.Q = p.f.colsw;
+    p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
+  }
+  int rc = finish_geo(p.f, d, false, p.K);
+  if (rc != SCAN2D_OK) return rc;
+  return finish_geo(p.b, d, true, p.K);
+}
+
+size_t slot_size(int dtype) { return dtype == SCAN2D_F64 ? 16 : 8; }
+
 struct WsLayout {
-  size_t flags = 0, hcarry = 0, rcarry = 0, part = 0, dbc = 0, total = 0;
+  size_t ticket = 0, hcarry = 0, rcarry = 0, part = 0, dbc = 0, total = 0;
 };
 
-// forward workspace: [flags][hcarry (when no residual is given)]
-// backward workspace: [flags][rcarry][part][per-scan dB, dC (G > 1)]
+// forward workspace: [ticket][hcarry (when no residual is given)]
+// backward workspace: [ticket][rcarry][part][per-scan dB, dC (G > 1)]
 WsLayout ws_layout(const scan2d_desc& d, const Plan& p, int op) {
-  const size_t es = dtype_size(d.dtype);
+  const size_t es = dtype_size(d.dtype), ss = slot_size(d.dtype);
   const size_t S = static_cast<size_t>(d.num_scans);
-  const size_t bnd = S * static_cast<size_t>(p.ncb - 1);
   WsLayout L;
   size_t off = 0;
-  L.flags = off;
-  off += align_up(sizeof(int) * (1 + bnd));
+  L.ticket = off;
+  off += kAlign;
   if (op == SCAN2D_OP_FWD) {
     L.hcarry = off;
-    off += align_up(es * bnd * d.height * d.state_dim);
+    off += align_up(ss * S * p.nq * d.height * d.state_dim);
   } else {
     L.rcarry = off;
-    off += align_up(es * bnd * d.height * d.state_dim);
+    off += align_up(ss * S * (p.b.wreal - 1) * d.height * d.state_dim);
     L.part = off;
-    off += align_up(es * S * p.wps * (d.state_dim + 2));
+    off += align_up(es * S * p.b.wreal * (d.state_dim + 2));
     if (d.bc_group > 1) {
       L.dbc = off;
       off += align_up(2 * es * S * d.height * d.width * d.state_dim);
@@ -126,16 +152,20 @@ struct ResLayout {
 };
 
 ResLayout res_layout(const scan2d_desc& d, const Plan& p) {
-  const size_t es = dtype_size(d.dtype);
+  const size_t es = dtype_size(d.dtype), ss = slot_size(d.dtype);
   const size_t S = static_cast<size_t>(d.num_scans);
   ResLayout R;
   R.ckpt = 0;
   size_t off = align_up(es * S * (p.nb - 1) * d.width * d.state_dim);
   R.hcarry = off;
-  off += align_up(es * S * (p.ncb - 1) * d.height * d.state_dim);
+  off += align_up(ss * S * p.nq * d.height * d.state_dim);
   R.total = std::max<size_t>(off, kAlign);
   return R;
 }
+
+std::atomic<uint32_t> g_epoch{0x9e3779b9u};
+
+uint32_t next_epoch(int H) { return g_epoch.fetch_add(static_cast<uint32_t>(H) + 1u); }
 
 int device_check() {
   int dev = 0;
@@ -153,19 +183,8 @@ int device_check() {
 }
 
 template <typename T>
-int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
-                 const void* A, const void* Dskip, const void* bias, void* y, void* ph, void* pv,
-                 void* residual, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  g_last_launches = 0;
-  if (!x || !z || !B || !C || !A || !Dskip || !bias || !y) return SCAN2D_EINVAL;
-  if ((ph == nullptr) != (pv == nullptr)) return SCAN2D_EINVAL;
-  int rc = device_check();
-  if (rc != SCAN2D_OK) return rc;
-  const Plan p = make_plan(d);
-  const WsLayout L = ws_layout(d, p, SCAN2D_OP_FWD);
-  if (ws_bytes < L.total || (L.total > 0 && ws == nullptr)) return SCAN2D_ENOMEM;
-  unsigned char* w = static_cast<unsigned char*>(ws);
-  Args<T> a{};
+void fill_common(Args<T>& a, const scan2d_desc& d, const Plan& p, const void* x, const void* z,
+                 const void* B, const void* C, const void* A, const void* Dskip, const void* bias) {
   a.x = static_cast<const T*>(x);
   a.z = static_cast<const T*>(z);
   a.B = static_cast<const T*>(B);
@@ -173,19 +192,6 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   a.A = static_cast<const T*>(A);
   a.Dskip = static_cast<const T*>(Dskip);
   a.bias = static_cast<const T*>(bias);
-  a.y = static_cast<T*>(y);
-  a.ph = static_cast<T*>(ph);
-  a.pv = static_cast<T*>(pv);
-  a.flags = reinterpret_cast<int*>(w + L.flags);
-  if (residual != nullptr) {
-    const ResLayout R = res_layout(d, p);
-    unsigned char* r = static_cast<unsigned char*>(residual);
-    a.ckpt = reinterpret_cast<T*>(r + R.ckpt);
-    a.hcarry = reinterpret_cast<T*>(r + R.hcarry);
-  } else {
-    a.ckpt = nullptr;
-    a.hcarry = reinterpret_cast<T*>(w + L.hcarry);
-  }
   a.S = d.num_scans;
   a.H = d.height;
   a.W = d.width;
@@ -194,17 +200,48 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   a.P = d.params_period;
   a.G = d.bc_group;
   a.plan = p;
-  if (p.ncb > 1) {
-    const size_t fb = sizeof(int) * (1 + static_cast<size_t>(d.num_scans) * (p.ncb - 1));
-    if (cudaMemsetAsync(a.flags, 0, fb, stream) != cudaSuccess) return SCAN2D_ECUDA;
+  a.epoch = next_epoch(d.height);
+}
+
+template <typename T>
+int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
+                 const void* A, const void* Dskip, const void* bias, void* y, void* ph, void* pv,
+                 void* residual, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  g_last_launches = 0;
+  if (!x || !z || !B || !C || !A || !Dskip || !bias || !y) return SCAN2D_EINVAL;
+  if ((ph == nullptr) != (pv == nullptr)) return SCAN2D_EINVAL;
+  int rc = device_check();
+  if (rc != SCAN2D_OK) return rc;
+  Plan p;
+  rc = make_plan(d, p);
+  if (rc != SCAN2D_OK) return rc;
+  const WsLayout L = ws_layout(d, p, SCAN2D_OP_FWD);
+  if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  Args<T> a{};
+  fill_common(a, d, p, x, z, B, C, A, Dskip, bias);
+  a.y = static_cast<T*>(y);
+  a.ph = static_cast<T*>(ph);
+  a.pv = static_cast<T*>(pv);
+  a.ticket = reinterpret_cast<int*>(w + L.ticket);
+  if (residual != nullptr) {
+    const ResLayout R = res_layout(d, p);
+    unsigned char* r = static_cast<unsigned char*>(residual);
+    a.ckpt = reinterpret_cast<T*>(r + R.ckpt);
+    a.hcarry = reinterpret_cast<s2d::CarrySlot<T>*>(r + R.hcarry);
+  } else {
+    a.ckpt = nullptr;
+    a.hcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.hcarry);
   }
+  if (p.f.wreal > 1 && cudaMemsetAsync(a.ticket, 0, sizeof(int), stream) != cudaSuccess)
+    return SCAN2D_ECUDA;
   if (ph != nullptr) {
     const size_t kh = ceil_div(d.height, d.tile), kw = ceil_div(d.width, d.tile);
     const size_t cb = sizeof(T) * static_cast<size_t>(d.num_scans) * kh * kw * d.tile * d.state_dim;
     if (cudaMemsetAsync(ph, 0, cb, stream) != cudaSuccess) return SCAN2D_ECUDA;
     if (cudaMemsetAsync(pv, 0, cb, stream) != cudaSuccess) return SCAN2D_ECUDA;
   }
-  if (s2d::launch_fwd<T>(a, s2d::fwd_smem_bytes<T>(p), stream) != cudaSuccess) return SCAN2D_ECUDA;
+  if (s2d::launch_fwd<T>(a, stream) != cudaSuccess) return SCAN2D_ECUDA;
   g_last_launches = 1;
   return SCAN2D_OK;
 }
@@ -221,23 +258,19 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   if (!dx || !dz || !dA || !dB || !dC || !dDskip || !dbias) return SCAN2D_EINVAL;
   int rc = device_check();
   if (rc != SCAN2D_OK) return rc;
-  const Plan p = make_plan(d);
+  Plan p;
+  rc = make_plan(d, p);
+  if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
   unsigned char* w = static_cast<unsigned char*>(ws);
   const ResLayout R = res_layout(d, p);
   const unsigned char* r = static_cast<const unsigned char*>(residual);
   Args<T> a{};
-  a.x = static_cast<const T*>(x);
-  a.z = static_cast<const T*>(z);
-  a.B = static_cast<const T*>(B);
-  a.C = static_cast<const T*>(C);
-  a.A = static_cast<const T*>(A);
-  a.Dskip = static_cast<const T*>(Dskip);
-  a.bias = static_cast<const T*>(bias);
+  fill_common(a, d, p, x, z, B, C, A, Dskip, bias);
   a.dy = static_cast<const T*>(dy);
   a.ckpt = const_cast<T*>(reinterpret_cast<const T*>(r + R.ckpt));
-  a.hcarry = const_cast<T*>(reinterpret_cast<const T*>(r + R.hcarry));
+  a.hcarry = const_cast<s2d::CarrySlot<T>*>(reinterpret_cast<const s2d::CarrySlot<T>*>(r + R.hcarry));
   a.dx = static_cast<T*>(dx);
   a.dz = static_cast<T*>(dz);
   T* dB_ps = static_cast<T*>(dB);
@@ -250,25 +283,15 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   a.dB = dB_ps;
   a.dC = dC_ps;
   a.part = reinterpret_cast<T*>(w + L.part);
-  a.rcarry = reinterpret_cast<T*>(w + L.rcarry);
-  a.flags = reinterpret_cast<int*>(w + L.flags);
-  a.S = d.num_scans;
-  a.H = d.height;
-  a.W = d.width;
-  a.N = d.state_dim;
-  a.T_tile = d.tile;
-  a.P = d.params_period;
-  a.G = d.bc_group;
-  a.plan = p;
-  if (p.ncb > 1) {
-    const size_t fb = sizeof(int) * (1 + static_cast<size_t>(d.num_scans) * (p.ncb - 1));
-    if (cudaMemsetAsync(a.flags, 0, fb, stream) != cudaSuccess) return SCAN2D_ECUDA;
-  }
+  a.rcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.rcarry);
+  a.ticket = reinterpret_cast<int*>(w + L.ticket);
+  if (p.b.wreal > 1 && cudaMemsetAsync(a.ticket, 0, sizeof(int), stream) != cudaSuccess)
+    return SCAN2D_ECUDA;
   int launches = 0;
-  if (s2d::launch_bwd<T>(a, s2d::bwd_smem_bytes<T>(p), stream) != cudaSuccess) return SCAN2D_ECUDA;
+  if (s2d::launch_bwd<T>(a, stream) != cudaSuccess) return SCAN2D_ECUDA;
   ++launches;
-  if (s2d::launch_reduce_params<T>(a.part, d.num_scans, p.wps, p.wreal, d.params_period,
-                                   d.state_dim, static_cast<T*>(dA), static_cast<T*>(dbias),
+  if (s2d::launch_reduce_params<T>(a.part, d.num_scans, p.b.wreal, d.params_period, d.state_dim,
+                                   static_cast<T*>(dA), static_cast<T*>(dbias),
                                    static_cast<T*>(dDskip), stream) != cudaSuccess)
     return SCAN2D_ECUDA;
   ++launches;
@@ -293,13 +316,15 @@ int scan2d_check_desc(const scan2d_desc* desc) { return check_desc(desc); }
 
 size_t scan2d_workspace_bytes(const scan2d_desc* desc, int op) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
-  const Plan p = make_plan(*desc);
+  Plan p;
+  if (make_plan(*desc, p) != SCAN2D_OK) return 0;
   return ws_layout(*desc, p, op).total;
 }
 
 size_t scan2d_residual_bytes(const scan2d_desc* desc) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
-  const Plan p = make_plan(*desc);
+  Plan p;
+  if (make_plan(*desc, p) != SCAN2D_OK) return 0;
   return res_layout(*desc, p).total;
 }
 
@@ -379,18 +404,20 @@ int scan2d_bwd_f64(const scan2d_desc* desc, const double* x, const double* z, co
 }
 
 int scan2d_plan_info(const scan2d_desc* desc, int op, int64_t* out8) {
-  const int rc = check_desc(desc);
+  int rc = check_desc(desc);
   if (rc != SCAN2D_OK) return rc;
   if (out8 == nullptr) return SCAN2D_EINVAL;
-  (void)op;
-  const Plan p = make_plan(*desc);
-  out8[0] = p.lpc;
-  out8[1] = p.J;
-  out8[2] = p.seg;
-  out8[3] = p.wps;
-  out8[4] = p.nw;
-  out8[5] = p.ncb;
-  out8[6] = p.ctas;
+  Plan p;
+  rc = make_plan(*desc, p);
+  if (rc != SCAN2D_OK) return rc;
+  const s2d::Geo& g = op == SCAN2D_OP_BWD ? p.b : p.f;
+  out8[0] = g.spl * 100 + g.lpc;  // states per lane * 100 + lanes per chunk
+  out8[1] = g.J;
+  out8[2] = g.seg;
+  out8[3] = g.wreal;
+  out8[4] = g.colsw;
+  out8[5] = g.smem_bytes;
+  out8[6] = g.units;
   out8[7] = p.K;
   return SCAN2D_OK;
 }

@@ -13,7 +13,6 @@
 namespace s2d {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kRing = 4;  // depth of the intra-CTA carry rings (rows in flight per hop)
 
 // ------------------------------------------------------------------ numerics
 
@@ -29,13 +28,33 @@ struct Num<float> {
     return r;
   }
   static __device__ __forceinline__ float a_scale(float a) { return a * 1.4426950408889634f; }
+  static __device__ __forceinline__ float rcp(float v) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+  }
+  // softplus(v) = max(v, 0) + log1p(exp(-|v|)), log1p(t) = 2 atanh(t / (2 + t)).
+  // With s = t/(2+t) in [0, 1/3], the odd atanh series to s^13 leaves a
+  // relative error < 2e-8; two MUFU ops (ex2, rcp) and ~14 FMA-pipe ops.
   static __device__ __forceinline__ float softplus(float v) {
-    return v > 20.0f ? v : log1pf(__expf(v));
+    const float t = exp_scaled(-fabsf(v) * 1.4426950408889634f);
+    const float s = t * rcp(2.0f + t);
+    const float s2 = s * s;
+    float p = 1.0f / 13.0f;
+    p = fmaf(p, s2, 1.0f / 11.0f);
+    p = fmaf(p, s2, 1.0f / 9.0f);
+    p = fmaf(p, s2, 1.0f / 7.0f);
+    p = fmaf(p, s2, 1.0f / 5.0f);
+    p = fmaf(p, s2, 1.0f / 3.0f);
+    p = fmaf(p, s2, 1.0f);
+    const float l1p = 2.0f * s * p;
+    const float r = fmaxf(v, 0.0f) + l1p;
+    return v > 20.0f ? v : r;
   }
   static __device__ __forceinline__ float sigmoid(float v) {
-    if (v >= 0.0f) return __frcp_rn(1.0f + __expf(-v));
-    const float e = __expf(v);
-    return e / (1.0f + e);
+    const float e = exp_scaled(-fabsf(v) * 1.4426950408889634f);  // exp(-|v|)
+    const float r = rcp(1.0f + e);
+    return v >= 0.0f ? r : e * r;
   }
 };
 
@@ -59,59 +78,117 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// mbarrier wrappers (CTA scope).  arrive has release semantics, try_wait acquire.
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+// cp.async (LDGSTS): global -> shared without staging through registers
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
                : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .b64 st;\n\t"
-      "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void cp_async_elem(float* smem, const float* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+__device__ __forceinline__ void cp_async_elem(double* smem, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
 }
-
-// ------------------------------------------------------ gpu-scope signalling
-
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+template <int NPending>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(NPending) : "memory");
 }
-__device__ __forceinline__ float ld_relaxed_gpu(const float* p) {
-  float v;
-  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ double ld_relaxed_gpu(const double* p) {
-  double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Spin (all lanes) until *flag > target; returns the observed value.
-__device__ __forceinline__ int wait_flag_gt(const int* flag, int target) {
-  int v = ld_acquire_gpu(flag);
-  while (v <= target) {
-    __nanosleep(32);
-    v = ld_acquire_gpu(flag);
+// wait until at most n committed groups are pending (n is warp-uniform)
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 4: cp_async_wait<4>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 6: cp_async_wait<6>(); break;
+    default: cp_async_wait<7>(); break;
   }
-  return v;
 }
+
+// Warp-cooperative copy of `count` contiguous elements into 16-byte aligned
+// shared memory: 16-byte LDGSTS where the source allows, element copies for
+// the rest.
+template <typename T>
+__device__ __forceinline__ void copy_span(T* dst, const T* src, int count, int lane) {
+  constexpr int EPV = 16 / sizeof(T);
+  int done = 0;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int nv = count / EPV;
+    for (int u = lane; u < nv; u += 32) cp_async16(dst + u * EPV, src + u * EPV);
+    done = nv * EPV;
+  }
+  for (int u = done + lane; u < count; u += 32) cp_async_elem(dst + u, src + u);
+}
+
+// ------------------------------------------------------ gpu-scope carries
+//
+// Tags are unique per (launch, row): the host advances `epoch` by H + 1 per
+// launch, so carry buffers never need clearing between launches; 0 never
+// occurs as a tag (fresh zeroed memory cannot be mistaken for a carry).
+__device__ __forceinline__ int row_tag(uint32_t epoch, int row) {
+  return static_cast<int>((epoch + static_cast<uint32_t>(row)) % 0x7fffffffu) + 1;
+}
+//
+// Column-group carries travel between warps (one warp per CTA) through global
+// memory.  fp32: the value and its row tag share one naturally aligned 8-byte
+// word, so a single relaxed store publishes both (no fence on the chain).
+// fp64: value, fence, then tag.
+
+template <typename T>
+struct CarrySlot;
+
+template <>
+struct CarrySlot<float> {
+  uint64_t w;
+  static __device__ __forceinline__ void put(CarrySlot* p, float v, int tag) {
+    const uint64_t w = (static_cast<uint64_t>(static_cast<uint32_t>(tag)) << 32) |
+                       static_cast<uint64_t>(__float_as_uint(v));
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(&p->w), "l"(w) : "memory");
+  }
+  static __device__ __forceinline__ float get_wait(const CarrySlot* p, int tag) {
+    uint64_t w;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(&p->w) : "memory");
+    while (static_cast<int>(w >> 32) != tag) {
+      __nanosleep(20);
+      asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(&p->w) : "memory");
+    }
+    return __uint_as_float(static_cast<uint32_t>(w));
+  }
+  static __device__ __forceinline__ float get(const CarrySlot* p) {
+    return __uint_as_float(static_cast<uint32_t>(p->w));
+  }
+};
+
+template <>
+struct CarrySlot<double> {
+  double v;
+  long long tag;
+  static __device__ __forceinline__ void put(CarrySlot* p, double v, int tag) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(&p->v), "d"(v) : "memory");
+    __threadfence();
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(&p->tag), "l"(static_cast<long long>(tag))
+                 : "memory");
+  }
+  static __device__ __forceinline__ double get_wait(const CarrySlot* p, int tag) {
+    long long t;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(t) : "l"(&p->tag) : "memory");
+    while (static_cast<int>(t) != tag) {
+      __nanosleep(20);
+      asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(t) : "l"(&p->tag) : "memory");
+    }
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(&p->v) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ double get(const CarrySlot* p) { return p->v; }
+};
 
 // ------------------------------------------------------- warp collectives
 
@@ -143,12 +220,11 @@ __device__ __forceinline__ int reduce_scatter(T (&v)[J], int l) {
   return colbase;
 }
 
-// columns each lane keeps after reduce_scatter, and the replica span
 template <int LPC, int J>
 struct RS {
   static constexpr int kKeep = (J / LPC) > 1 ? (J / LPC) : 1;
-  static constexpr int kDistinct = J / kKeep;        // distinct column groups per chunk
-  static constexpr int kReplica = LPC / kDistinct;   // lanes holding the same columns
+  static constexpr int kDistinct = J / kKeep;
+  static constexpr int kReplica = LPC / kDistinct;
 };
 
 template <int J, typename T>
@@ -160,31 +236,85 @@ __device__ __forceinline__ T select_col(const T (&v)[J], int k) {
   return r;
 }
 
-// butterfly sum over the lane bits in [lo_bit_mask .. 32) selected by `mask_bits`
-template <typename T>
-__device__ __forceinline__ T xor_sum(T v, int first, int last_exclusive) {
-  for (int h = first; h < last_exclusive; h <<= 1) v += __shfl_xor_sync(kFull, v, h);
-  return v;
+// SPL consecutive states of one cell from shared memory
+template <typename T, int SPL>
+__device__ __forceinline__ void lds_states(T (&out)[SPL], const T* p, bool vec) {
+  if constexpr (SPL == 4 && sizeof(T) == 4) {
+    if (vec) {
+      const float4 v = *reinterpret_cast<const float4*>(p);
+      out[0] = v.x;
+      out[1] = v.y;
+      out[2] = v.z;
+      out[3] = v.w;
+      return;
+    }
+  }
+  if constexpr (SPL == 2 && sizeof(T) == 4) {
+    if (vec) {
+      const float2 v = *reinterpret_cast<const float2*>(p);
+      out[0] = v.x;
+      out[1] = v.y;
+      return;
+    }
+  }
+  if constexpr (SPL >= 2 && sizeof(T) == 8) {
+    if (vec) {
+#pragma unroll
+      for (int s = 0; s < SPL; s += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(p + s);
+        out[s] = v.x;
+        out[s + 1] = v.y;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < SPL; ++s) out[s] = p[s];
+}
+
+template <typename T, int SPL>
+__device__ __forceinline__ void stg_states(T* p, const T (&v)[SPL], int nvalid, bool vec) {
+  if constexpr (SPL == 4 && sizeof(T) == 4) {
+    if (vec) {
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+      return;
+    }
+  }
+  if constexpr (SPL == 2 && sizeof(T) == 4) {
+    if (vec) {
+      *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < SPL; ++s)
+    if (s < nvalid) p[s] = v[s];
 }
 
 // ---------------------------------------------------------------- planning
 
-// Launch geometry shared by host and device (see scan2d_capi.cu: make_plan).
-struct Plan {
-  int lpc;      // lanes per chunk = state lanes (power of two <= 32)
-  int J;        // columns per chunk (per lane)
-  int cpw;      // chunks per warp = 32 / lpc
-  int seg;      // scans packed per warp (power of two; 1 when a scan spans >= 1 warp)
+// Geometry of one kernel direction.  A warp owns `colsw` columns of one scan
+// (or `seg` whole narrow scans); lanes = (chunk, state group): SPL states of
+// J consecutive columns per lane, LPC lanes per chunk, CPW = 32/LPC chunks.
+struct Geo {
+  int spl, lpc, cpw, J;
+  int seg;      // scans packed per warp (power of two)
   int cps;      // chunks per segment = cpw / seg
-  int wps;      // warps per scan (padded: nw * ncb) -- 1 when seg > 1
-  int wreal;    // warps per scan that own at least one real column
-  int nw;       // warps per CTA
-  int ncb;      // CTAs across one scan's width (cross-CTA carry chain when > 1)
-  int K;        // backward band rows (= checkpoint interval of the residual)
-  int nb;       // ceil(H / K)
-  int64_t units;  // logical warps = ceil(S / seg) * wps
-  int64_t ctas;
   int colsw;    // columns per warp (per segment)
+  int wreal;    // warps per scan with at least one real column
+  int stages;   // depth of the cp.async row pipeline
+  int64_t units;  // warps (= CTAs) in the launch
+  int stage_elems;  // elements per pipeline stage
+  int smem_bytes;   // dynamic shared memory per CTA
+};
+
+struct Plan {
+  Geo f;      // forward
+  Geo b;      // backward
+  int K;      // backward band rows (= residual checkpoint interval)
+  int nb;     // ceil(H / K)
+  int Q;      // column interval of the saved horizontal carries (= b.colsw)
+  int nq;     // ceil(W / Q) - 1 carry boundaries per row
 };
 
 template <typename T>
@@ -202,16 +332,17 @@ struct Args {
   T* y;
   T* ph;
   T* pv;
-  T* ckpt;     // residual: h at the last row of each band but the last, [S][nb-1][W][N]
-  T* hcarry;   // horizontal carry at CTA boundaries, [S][ncb-1][H][N]
+  T* ckpt;              // residual: h at the last row of each band but the last, [S][nb-1][W][N]
+  CarrySlot<T>* hcarry; // horizontal carry at every Q-column boundary, [S][nq][H][N]
   // backward outputs
   T* dx;
   T* dz;
   T* dB;       // [S][H][W][N] (per scan; reduced over the B/C group afterwards when G > 1)
   T* dC;
-  T* part;     // per (scan, warp) partials: [S][wps][N + 2] = dA[N], dbias, dD
-  T* rcarry;   // reverse carry at CTA boundaries, [S][ncb-1][H][N]
-  int* flags;  // [0] ticket, [1 + s*(ncb-1) + cb] progress of boundary cb of scan s
+  T* part;     // per (scan, warp) partials: [S][wreal_b][N + 2] = dA[N], dbias, dD
+  CarrySlot<T>* rcarry;  // reverse carry at backward warp boundaries, [S][wreal_b-1][H][N]
+  int* ticket;           // warp ticket counter (zeroed before each chained launch)
+  uint32_t epoch;        // tag base of this launch (see row_tag)
   // shape
   int64_t S;
   int H, W, N, T_tile, P, G;

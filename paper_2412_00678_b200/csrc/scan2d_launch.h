@@ -9,20 +9,21 @@
 
 namespace s2d {
 
-// Returns cudaSuccess or the launch error.  Kernels are picked by (lpc, J).
+// Returns cudaSuccess or the launch error.  Kernels are picked by (spl, lpc, J).
 template <typename T>
-cudaError_t launch_fwd(const Args<T>& a, size_t smem_bytes, cudaStream_t stream);
+cudaError_t launch_fwd(const Args<T>& a, cudaStream_t stream);
 template <typename T>
-cudaError_t launch_bwd(const Args<T>& a, size_t smem_bytes, cudaStream_t stream);
+cudaError_t launch_bwd(const Args<T>& a, cudaStream_t stream);
 template <typename T>
-cudaError_t launch_reduce_params(const T* part, int64_t S, int wps, int wreal, int P, int N, T* dA,
-                                 T* dbias, T* dD, cudaStream_t stream);
+cudaError_t launch_reduce_params(const T* part, int64_t S, int wps, int P, int N, T* dA, T* dbias,
+                                 T* dD, cudaStream_t stream);
 template <typename T>
 cudaError_t launch_reduce_group(const T* per_scan, int64_t groups, int G, size_t hwn, T* out,
                                 cudaStream_t stream);
+// shared-memory geometry (elements of T)
 template <typename T>
-size_t fwd_smem_bytes(const Plan& p);
+int stage_elems(int colsw, int N, int seg, bool bwd);
 template <typename T>
-size_t bwd_smem_bytes(const Plan& p);
+int band_elems(int K, int J, int SPL);
 
 }  // namespace s2d
