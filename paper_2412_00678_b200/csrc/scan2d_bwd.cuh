@@ -63,13 +63,12 @@ __host__ __device__ inline int bwd_band_elems(int K, int J, int SPL) {
 
 template <typename T, int SPL, int LPC, int J>
 __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
-  constexpr int CPW = 32 / LPC;
   constexpr int DPL = (J + LPC - 1) / LPC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   const Geo& ge = a.plan.b;
   const int lane = threadIdx.x;
-  const int H = a.H, W = a.W, N = a.N;
+  const int H = a.H, W = a.W, N = a.N, Np = ge.Np;
   const int K = a.plan.K, nb = a.plan.nb;
 
   int64_t unit = blockIdx.x;
@@ -81,36 +80,19 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
     const int64_t ss = t / ge.wreal;
     unit = ss * ge.wreal + (ge.wreal - 1 - t % ge.wreal);
   }
-  const int q = lane % LPC;
-  const int c = lane / LPC;
-  const int segw = 32 / ge.seg;
-  const int lane_in_seg = lane & (segw - 1);
-  const int gseg = c / ge.cps;
-  const int cis = c % ge.cps;
-  int64_t s;
-  int wpos;
-  if (ge.seg > 1) {
-    s = unit * ge.seg + gseg;
-    wpos = 0;
-  } else {
-    s = unit / ge.wreal;
-    wpos = static_cast<int>(unit % ge.wreal);
-  }
-  const bool scan_ok = s < a.S;
-  const int64_t sc = scan_ok ? s : 0;
-  const int c0 = wpos * ge.colsw;
-  const int colc = c0 + cis * J;
+  const LaneMap lm = lane_map<LPC, J>(ge, unit, lane, a.S, W);
+  const int q = lm.q, cis = lm.cis, segw = lm.segw, lane_in_seg = lm.lane_in_seg;
+  const int64_t sc = lm.scan_ok ? lm.s : 0;
   const int p = static_cast<int>(sc % a.P);
   const size_t HW = static_cast<size_t>(H) * W;
-  const bool vec = (N % SPL) == 0;
+  const int nvalid = N - q * SPL;
+  const bool svec = nvalid >= SPL && (N % SPL) == 0;  // vector global stores of the lane's states
 
   T A2[SPL], Ad[SPL];
-  bool dok[SPL];
 #pragma unroll
   for (int e = 0; e < SPL; ++e) {
     const int d = q * SPL + e;
-    dok[e] = scan_ok && d < N;
-    Ad[e] = dok[e] ? a.A[static_cast<int64_t>(p) * N + d] : T(0);
+    Ad[e] = (lm.scan_ok && d < N) ? a.A[static_cast<int64_t>(p) * N + d] : T(0);
     A2[e] = Num<T>::a_scale(Ad[e]);
   }
   const T Dsk = a.Dskip[p], bias = a.bias[p];
@@ -119,43 +101,37 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   T* hb = smem + static_cast<size_t>(nstage) * ge.stage_elems;  // [(K+1)][J][32][SPL]
   T* ec = hb + static_cast<size_t>(K + 1) * J * 32 * SPL;        // [K][32][SPL]
   for (int e = lane; e < nstage * ge.stage_elems; e += 32) smem[e] = T(0);
-  __syncwarp();
 
-  const StageLayout<T> Ls(ge.colsw, N, true);
-  auto issue = [&](int t, int st) {
-    const Job jb = job_of(t, H, K, nb);
-    T* dst0 = smem + static_cast<size_t>(st) * ge.stage_elems;
-    for (int g = 0; g < ge.seg; ++g) {
-      const int64_t sg = ge.seg > 1 ? unit * ge.seg + g : s;
-      if (sg >= a.S) break;
-      const int ncols = min(ge.colsw, W - c0);
-      if (ncols <= 0) break;
-      T* dst = dst0 + g * Ls.seg_stride;
-      const size_t ro = (static_cast<size_t>(sg) * H + jb.row) * W + c0;
-      copy_span(dst + Ls.xo, a.x + ro, ncols, lane);
-      copy_span(dst + Ls.zo, a.z + ro, ncols, lane);
-      const size_t bo = ((static_cast<size_t>(sg / a.G) * H + jb.row) * W + c0) * N;
-      copy_span(dst + Ls.bo, a.B + bo, ncols * N, lane);
-      if (jb.isR) {
-        copy_span(dst + Ls.dyo, a.dy + ro, ncols, lane);
-        copy_span(dst + Ls.co, a.C + bo, ncols * N, lane);
-      }
-    }
-  };
+  const StageLayout<T> Ls(ge.colsw, Np, true);
+  Stager<T> stg;
+  stg.xvec = a.xvec != 0;
+  stg.bvec = a.bvec != 0;
+  stg.zoff = Ls.zo - Ls.xo;
+  stg.dyoff = Ls.dyo - Ls.xo;
+  stg.coff = Ls.co - Ls.bo;
+  stg.x0 = a.x + lm.s0 * HW;
+  stg.z0 = a.z + lm.s0 * HW;
+  stg.dy0 = a.dy + lm.s0 * HW;
+  stg.B0 = a.B + (lm.s0 / a.G) * HW * N;
+  stg.C0 = a.C + (lm.s0 / a.G) * HW * N;
+  stg.xstride = W;
+  stg.bstride = static_cast<size_t>(W) * N;
+  stg.build(reinterpret_cast<CopyEntry*>(smem + ge.table_off), lane, lm.seg_scans, lm.c0, lm.ncols, N, Np,
+            HW, Ls, lm.s0, a.G);
 
   const int nbm1 = nb - 1, Q = a.plan.Q, nq = a.plan.nq;
-  const bool has_pred = wpos > 0;
-  const bool has_succ = wpos + 1 < ge.wreal;
+  const bool has_pred = lm.wpos > 0;
+  const bool has_succ = lm.wpos + 1 < ge.wreal;
   // saved forward carry into this warp's first column (residual, no waiting)
-  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((sc * nq + (c0 / Q - 1)) * H) * N : nullptr;
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((sc * nq + (lm.c0 / Q - 1)) * H) * N + q * SPL : nullptr;
   // reverse chain: receive from wpos+1, send to wpos-1 ([S][wreal-1][H][N])
   const int wb = ge.wreal - 1;
-  const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((sc * wb + wpos) * H) * N : nullptr;
-  CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((sc * wb + (wpos - 1)) * H) * N : nullptr;
+  const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((sc * wb + lm.wpos) * H) * N + q * SPL : nullptr;
+  CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((sc * wb + (lm.wpos - 1)) * H) * N + q * SPL : nullptr;
   T* dxs = a.dx + sc * HW;
   T* dzs = a.dz + sc * HW;
-  T* dBs = a.dB + sc * HW * N;
-  T* dCs = a.dC + sc * HW * N;
+  T* dBs = a.dB + sc * HW * N + q * SPL;
+  T* dCs = a.dC + sc * HW * N + q * SPL;
 
   T dn[J][SPL];  // Abar(i+1) G(i+1): the reverse vertical state (engine.cpp:323)
   T hv[J][SPL];  // forward vertical state during phase F
@@ -171,9 +147,13 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   for (int e = 0; e < SPL; ++e) dA_acc[e] = T(0);
   T dbias_acc = T(0), dD_acc = T(0);
 
+  __syncwarp();
   const int njobs = 2 * H;
   for (int t = 0; t < nstage - 1; ++t) {
-    if (t < njobs) issue(t, t);
+    if (t < njobs) {
+      const Job jb = job_of(t, H, K, nb);
+      stg.issue(smem + t * ge.stage_elems, jb.row, lane, jb.isR, jb.isR);
+    }
     cp_async_commit();
   }
   int st = 0;
@@ -182,12 +162,15 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
       const int tn = t + nstage - 1;
       int sn = st + nstage - 1;
       if (sn >= nstage) sn -= nstage;
-      if (tn < njobs) issue(tn, sn);
+      if (tn < njobs) {
+        const Job jn = job_of(tn, H, K, nb);
+        stg.issue(smem + sn * ge.stage_elems, jn.row, lane, jn.isR, jn.isR);
+      }
       cp_async_commit();
     }
     cp_async_wait_dyn(nstage - 1);
     __syncwarp();
-    const T* stg = smem + static_cast<size_t>(st) * ge.stage_elems + gseg * Ls.seg_stride;
+    const T* sx = smem + st * ge.stage_elems + lm.gseg * Ls.seg_stride;
     const Job jb = job_of(t, H, K, nb);
     const int i = jb.row;
     const int rb = i - jb.r0;  // row within the band
@@ -197,50 +180,39 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
 #pragma unroll
     for (int m = 0; m < DPL; ++m) {
       const int kk = q + m * LPC;
-      const T v = kk < J ? stg[Ls.zo + cis * J + kk] + bias : T(0);
+      const T v = kk < J ? sx[Ls.zo + cis * J + kk] + bias : T(0);
       dl[m] = Num<T>::softplus(v);
       sl[m] = jb.isR ? Num<T>::sigmoid(v) : T(0);
     }
-    T delta[J], sig[J];
+    T delta[J];
     const int base_lane = lane & ~(LPC - 1);
 #pragma unroll
-    for (int k = 0; k < J; ++k) {
-      delta[k] = __shfl_sync(kFull, dl[k / LPC], base_lane + (k % LPC));
-      sig[k] = __shfl_sync(kFull, sl[k / LPC], base_lane + (k % LPC));
-    }
-    T av[J][SPL], uv[J][SPL], bq[J][SPL];
+    for (int k = 0; k < J; ++k) delta[k] = __shfl_sync(kFull, dl[k / LPC], base_lane + (k % LPC));
+    T av[J][SPL], uv[J][SPL];
 #pragma unroll
     for (int k = 0; k < J; ++k) {
       const int col = cis * J + k;
-      const bool okc = scan_ok && (c0 + col) < W;
-      const T xk = stg[Ls.xo + col];
-      lds_states<T, SPL>(bq[k], stg + Ls.bo + col * N + q * SPL, vec);
+      const T xk = sx[Ls.xo + col];
+      T bq[SPL];
+      lds_states<T, SPL>(bq, sx + Ls.bo + col * Np + q * SPL, true);
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
-        const bool ok = okc && dok[e];
-        av[k][e] = ok ? Num<T>::exp_scaled(delta[k] * A2[e]) : T(1);
-        uv[k][e] = ok ? (delta[k] * bq[k][e]) * xk : T(0);
-        if (!ok) bq[k][e] = T(0);
+        av[k][e] = Num<T>::exp_scaled(delta[k] * A2[e]);
+        uv[k][e] = (delta[k] * bq[e]) * xk;
       }
     }
 
     if (!jb.isR) {
       // ================================================= phase F (recompute)
       if (rb == 0) {
-        T* h0 = hb;  // row -1 of the band: the checkpoint
+        const T* ck = a.ckpt + ((static_cast<size_t>(sc) * nbm1 + (jb.r0 / K - 1)) * W) * N + q * SPL;
 #pragma unroll
         for (int k = 0; k < J; ++k) {
-          const int j = colc + k;
-          T v[SPL];
-#pragma unroll
-          for (int e = 0; e < SPL; ++e) v[e] = T(0);
-          if (jb.r0 > 0 && scan_ok && j < W)
-            lds_states<T, SPL>(v, a.ckpt + ((static_cast<size_t>(sc) * nbm1 + (jb.r0 / K - 1)) * W + j) * N + q * SPL,
-                               false);
+          const int j = lm.colc + k;
 #pragma unroll
           for (int e = 0; e < SPL; ++e) {
-            hv[k][e] = dok[e] ? v[e] : T(0);
-            h0[(k * 32 + lane) * SPL + e] = hv[k][e];
+            hv[k][e] = (jb.r0 > 0 && lm.scan_ok && j < W && e < nvalid) ? ck[static_cast<size_t>(j) * N + e] : T(0);
+            hb[(k * 32 + lane) * SPL + e] = hv[k][e];
           }
         }
       }
@@ -274,6 +246,13 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
           }
         }
       }
+      T ew[SPL];
+      if (has_pred)
+        carry_get<T, SPL>(hc_in + static_cast<size_t>(i) * N, ew, nvalid);
+      else {
+#pragma unroll
+        for (int e = 0; e < SPL; ++e) ew[e] = T(0);
+      }
       T hh[SPL];
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
@@ -283,9 +262,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
           Pe = T(1);
           Le = T(0);
         }
-        const T ew = (has_pred && dok[e]) ? CarrySlot<T>::get(hc_in + static_cast<size_t>(i) * N + q * SPL + e)
-                                          : T(0);
-        hh[e] = fma(Pe, ew, Le);
+        hh[e] = fma(Pe, ew[e], Le);
         ec[(rb * 32 + lane) * SPL + e] = hh[e];
       }
       T* hrow = hb + static_cast<size_t>(rb + 1) * J * 32 * SPL;
@@ -299,42 +276,42 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
         }
     } else {
       // ================================================= phase R (adjoints)
-      T G[J][SPL], dyk[J];
+      T sig[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) sig[k] = __shfl_sync(kFull, sl[k / LPC], base_lane + (k % LPC));
+      T G[J][SPL];
 #pragma unroll
       for (int k = 0; k < J; ++k) {
         const int col = cis * J + k;
-        dyk[k] = stg[Ls.dyo + col];
+        const T dyk = sx[Ls.dyo + col];
         T cq[SPL];
-        lds_states<T, SPL>(cq, stg + Ls.co + col * N + q * SPL, vec);
-        const bool okc = scan_ok && (c0 + col) < W;
+        lds_states<T, SPL>(cq, sx + Ls.co + col * Np + q * SPL, true);
 #pragma unroll
-        for (int e = 0; e < SPL; ++e) G[k][e] = fma((okc && dok[e]) ? cq[e] : T(0), dyk[k], dn[k][e]);
+        for (int e = 0; e < SPL; ++e) G[k][e] = fma(cq[e], dyk, dn[k][e]);  // engine.cpp:321
       }
       // chunk reverse map rho_out = al rho_in + be (engine.cpp:343-350)
       T al[SPL], be[SPL];
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
-        T r = T(0);
-        T prod = T(1);
+        T r = T(0), pr = T(1);
 #pragma unroll
         for (int k = J - 1; k >= 0; --k) {
           r = av[k][e] * (G[k][e] + r);
-          prod = prod * av[k][e];
+          pr = pr * av[k][e];
         }
-        al[e] = prod;
+        al[e] = pr;
         be[e] = r;
       }
-      const int span = segw;
 #pragma unroll
       for (int off = LPC; off < 32; off <<= 1) {
-        if (off >= span) break;
+        if (off >= segw) break;
         T ad[SPL], bd[SPL];
 #pragma unroll
         for (int e = 0; e < SPL; ++e) {
           ad[e] = __shfl_down_sync(kFull, al[e], off, segw);
           bd[e] = __shfl_down_sync(kFull, be[e], off, segw);
         }
-        if (lane_in_seg + off < span) {
+        if (lane_in_seg + off < segw) {
 #pragma unroll
           for (int e = 0; e < SPL; ++e) {
             be[e] = fma(al[e], bd[e], be[e]);
@@ -346,11 +323,9 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
       {
         T rw[SPL];
 #pragma unroll
-        for (int e = 0; e < SPL; ++e) {
-          rw[e] = (has_succ && dok[e])
-                      ? CarrySlot<T>::get_wait(rc_in + static_cast<size_t>(i) * N + q * SPL + e, row_tag(a.epoch, i))
-                      : T(0);
-        }
+        for (int e = 0; e < SPL; ++e) rw[e] = T(0);
+        const int tag = row_tag(a.epoch, i);
+        if (has_succ) carry_get_wait<T, SPL>(rc_in + static_cast<size_t>(i) * N, rw, tag, nvalid);
         if (has_pred) {
           T out[SPL];
 #pragma unroll
@@ -359,18 +334,13 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
             const T bt = __shfl_sync(kFull, be[e], q);
             out[e] = fma(at, rw[e], bt);
           }
-          if (c == 0) {
-#pragma unroll
-            for (int e = 0; e < SPL; ++e)
-              if (dok[e])
-                CarrySlot<T>::put(rc_out + static_cast<size_t>(i) * N + q * SPL + e, out[e], row_tag(a.epoch, i));
-          }
+          if (lm.c == 0) carry_put<T, SPL>(rc_out + static_cast<size_t>(i) * N, out, tag, nvalid);
         }
 #pragma unroll
         for (int e = 0; e < SPL; ++e) {
           T ae = __shfl_down_sync(kFull, al[e], LPC, segw);
           T bx = __shfl_down_sync(kFull, be[e], LPC, segw);
-          if (lane_in_seg + LPC >= span) {
+          if (lane_in_seg + LPC >= segw) {
             ae = T(1);
             bx = T(0);
           }
@@ -395,41 +365,43 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
       const size_t rowb = static_cast<size_t>(i) * W;
 #pragma unroll
       for (int k = 0; k < J; ++k) {
-        const int j = colc + k;
-        const bool okc = scan_ok && j < W;
-        const T xk = stg[Ls.xo + cis * J + k];
-        T hu[SPL], hc[SPL], dBv[SPL], dCv[SPL];
+        const int col = cis * J + k;
+        const int j = lm.colc + k;
+        const T xk = sx[Ls.xo + col], dyk = sx[Ls.dyo + col];
+        T bq[SPL], hu[SPL], hc[SPL], dBv[SPL], dCv[SPL];
+        lds_states<T, SPL>(bq, sx + Ls.bo + col * Np + q * SPL, true);
         lds_states<T, SPL>(hu, hup + (k * 32 + lane) * SPL, true);
         lds_states<T, SPL>(hc, hcur + (k * 32 + lane) * SPL, true);
         T dd = T(0), sg = T(0);
+        const T dax = delta[k] * xk;
 #pragma unroll
         for (int e = 0; e < SPL; ++e) {
           const T dab = fma(Gh[k][e], hl[e], G[k][e] * hu[e]);
           hl[e] = fma(av[k][e], hl[e], uv[k][e]);
-          if (okc && dok[e]) dA_acc[e] = fma(dab, delta[k] * av[k][e], dA_acc[e]);
-          dd = fma(Gh[k][e], bq[k][e] * xk, fma(dab, av[k][e] * Ad[e], dd));
-          sg = fma(Gh[k][e], bq[k][e], sg);
-          dBv[e] = Gh[k][e] * (delta[k] * xk);
-          dCv[e] = dyk[k] * hc[e];
+          dA_acc[e] = fma(dab, delta[k] * av[k][e], dA_acc[e]);
+          dd = fma(Gh[k][e], bq[e] * xk, fma(dab, av[k][e] * Ad[e], dd));
+          sg = fma(Gh[k][e], bq[e], sg);
+          dBv[e] = Gh[k][e] * dax;
+          dCv[e] = dyk * hc[e];
           dn[k][e] = av[k][e] * G[k][e];
         }
         ddp[k] = dd;
         sgb[k] = sg;
-        if (okc && q * SPL < N) {
-          stg_states<T, SPL>(dBs + (rowb + j) * N + q * SPL, dBv, N - q * SPL, vec);
-          stg_states<T, SPL>(dCs + (rowb + j) * N + q * SPL, dCv, N - q * SPL, vec);
+        if (lm.scan_ok && j < W && nvalid > 0) {
+          stg_states<T, SPL>(dBs + (rowb + j) * N, dBv, nvalid, svec);
+          stg_states<T, SPL>(dCs + (rowb + j) * N, dCv, nvalid, svec);
         }
       }
       using RS_ = RS<LPC, J>;
       const int cbase = reduce_scatter<LPC, J>(ddp, q);
       reduce_scatter<LPC, J>(sgb, q);
-      if ((q & (RS_::kReplica - 1)) == 0 && scan_ok) {
+      if ((q & (RS_::kReplica - 1)) == 0 && lm.scan_ok) {
 #pragma unroll
         for (int m = 0; m < RS_::kKeep; ++m) {
           const int k = cbase + m;
-          const int j = colc + k;
+          const int j = lm.colc + k;
           if (j < W) {
-            const T dyv = stg[Ls.dyo + cis * J + k], xv = stg[Ls.xo + cis * J + k];
+            const T dyv = sx[Ls.dyo + cis * J + k], xv = sx[Ls.xo + cis * J + k];
             const T dv = select_col<J>(delta, k), sv = select_col<J>(sig, k);
             const T dzv = ddp[m] * sv;
             dxs[rowb + j] = fma(Dsk, dyv, dv * sgb[m]);
@@ -452,12 +424,12 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
     dbias_acc += __shfl_xor_sync(kFull, dbias_acc, h);
     dD_acc += __shfl_xor_sync(kFull, dD_acc, h);
   }
-  if (scan_ok) {
-    T* part = a.part + (static_cast<size_t>(s) * ge.wreal + wpos) * (N + 2);
+  if (lm.scan_ok) {
+    T* part = a.part + (static_cast<size_t>(lm.s) * ge.wreal + lm.wpos) * (N + 2);
     if (lane_in_seg < LPC) {
 #pragma unroll
       for (int e = 0; e < SPL; ++e)
-        if (dok[e]) part[q * SPL + e] = dA_acc[e];
+        if (e < nvalid) part[q * SPL + e] = dA_acc[e];
     }
     if (lane_in_seg == 0) {
       part[N] = dbias_acc;

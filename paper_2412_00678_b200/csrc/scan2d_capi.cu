@@ -55,6 +55,7 @@ s2d::Geo make_geo(const scan2d_desc& d, bool bwd) {
   const int Np = next_pow2(N);
   g.spl = Np >= 4 ? 4 : Np;
   g.lpc = Np / g.spl;
+  g.Np = Np;
   g.cpw = 32 / g.lpc;
   if (g.spl == 4)
     g.J = bwd ? 2 : 4;
@@ -76,13 +77,21 @@ s2d::Geo make_geo(const scan2d_desc& d, bool bwd) {
   return g;
 }
 
-int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K) {
+// Shared memory: pipeline stages, backward band storage, then the copy table.
+// The table size depends on whether 16-byte copy units are legal (vec flags).
+int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K, bool xvec, bool bvec) {
   const bool dbl = d.dtype == SCAN2D_F64;
-  g.stage_elems = dbl ? s2d::stage_elems<double>(g.colsw, d.state_dim, g.seg, bwd)
-                      : s2d::stage_elems<float>(g.colsw, d.state_dim, g.seg, bwd);
+  const int es = static_cast<int>(dtype_size(d.dtype));
+  g.stage_elems = dbl ? s2d::stage_elems<double>(g.colsw, g.Np, g.seg, bwd)
+                      : s2d::stage_elems<float>(g.colsw, g.Np, g.seg, bwd);
   size_t elems = static_cast<size_t>(g.stages) * g.stage_elems;
   if (bwd) elems += dbl ? s2d::band_elems<double>(K, g.J, g.spl) : s2d::band_elems<float>(K, g.J, g.spl);
-  const size_t bytes = elems * dtype_size(d.dtype);
+  g.table_off = static_cast<int>(elems);
+  const int epv = 16 / es;
+  const int ncols = std::min<int>(g.colsw, d.width);
+  const int nx = s2d::stage_units_x(g.seg, ncols, xvec, epv);
+  const int nbu = s2d::stage_units_b(g.seg, ncols, d.state_dim, bvec, epv);
+  const size_t bytes = elems * es + static_cast<size_t>(nx + nbu) * 32 * sizeof(s2d::CopyEntry);
   if (bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
   g.smem_bytes = static_cast<int>(bytes);
   return SCAN2D_OK;
@@ -110,9 +119,31 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     p.Q = p.f.colsw;
     p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
   }
-  int rc = finish_geo(p.f, d, false, p.K);
+  return SCAN2D_OK;
+}
+
+// 16-byte copy units are legal when every span of every row starts 16-byte
+// aligned: base pointers aligned and all row / column offsets multiples of 16 B.
+void vec_flags(const scan2d_desc& d, const Plan& p, const void* x, const void* z, const void* dy,
+               const void* B, const void* C, const void* y, bool& xvec, bool& bvec, bool& yvec) {
+  const int es = static_cast<int>(dtype_size(d.dtype));
+  const int epv = 16 / es;
+  auto al = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool cols_ok = (p.f.colsw % epv) == 0 && (p.b.colsw % epv) == 0;
+  xvec = al(x) && al(z) && al(dy) && (d.width % epv) == 0 && cols_ok;
+  bvec = al(B) && al(C) && next_pow2(d.state_dim) == d.state_dim &&
+         (static_cast<int64_t>(d.width) * d.state_dim) % epv == 0 &&
+         (static_cast<int64_t>(p.f.colsw) * d.state_dim) % epv == 0 &&
+         (static_cast<int64_t>(p.b.colsw) * d.state_dim) % epv == 0;
+  yvec = al(y) && (d.width % 4) == 0;
+}
+
+int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
+  int rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
-  return finish_geo(p.b, d, true, p.K);
+  rc = finish_geo(p.f, d, false, p.K, xvec, bvec);
+  if (rc != SCAN2D_OK) return rc;
+  return finish_geo(p.b, d, true, p.K, xvec, bvec);
 }
 
 size_t slot_size(int dtype) { return dtype == SCAN2D_F64 ? 16 : 8; }
@@ -204,6 +235,13 @@ void fill_common(Args<T>& a, const scan2d_desc& d, const Plan& p, const void* x,
 }
 
 template <typename T>
+void set_flags(Args<T>& a, bool xvec, bool bvec, bool yvec) {
+  a.xvec = xvec;
+  a.bvec = bvec;
+  a.yvec = yvec;
+}
+
+template <typename T>
 int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
                  const void* A, const void* Dskip, const void* bias, void* y, void* ph, void* pv,
                  void* residual, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -215,11 +253,16 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   Plan p;
   rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
+  bool xvec, bvec, yvec;
+  vec_flags(d, p, x, z, nullptr, B, C, y, xvec, bvec, yvec);
+  rc = plan_with_flags(d, p, xvec, bvec);
+  if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_FWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
   unsigned char* w = static_cast<unsigned char*>(ws);
   Args<T> a{};
   fill_common(a, d, p, x, z, B, C, A, Dskip, bias);
+  set_flags(a, xvec, bvec, yvec);
   a.y = static_cast<T*>(y);
   a.ph = static_cast<T*>(ph);
   a.pv = static_cast<T*>(pv);
@@ -261,6 +304,10 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   Plan p;
   rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
+  bool xvec, bvec, yvec;
+  vec_flags(d, p, x, z, dy, B, C, nullptr, xvec, bvec, yvec);
+  rc = plan_with_flags(d, p, xvec, bvec);
+  if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
   unsigned char* w = static_cast<unsigned char*>(ws);
@@ -268,6 +315,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   const unsigned char* r = static_cast<const unsigned char*>(residual);
   Args<T> a{};
   fill_common(a, d, p, x, z, B, C, A, Dskip, bias);
+  set_flags(a, xvec, bvec, yvec);
   a.dy = static_cast<const T*>(dy);
   a.ckpt = const_cast<T*>(reinterpret_cast<const T*>(r + R.ckpt));
   a.hcarry = const_cast<s2d::CarrySlot<T>*>(reinterpret_cast<const s2d::CarrySlot<T>*>(r + R.hcarry));
@@ -317,14 +365,14 @@ int scan2d_check_desc(const scan2d_desc* desc) { return check_desc(desc); }
 size_t scan2d_workspace_bytes(const scan2d_desc* desc, int op) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
   Plan p;
-  if (make_plan(*desc, p) != SCAN2D_OK) return 0;
+  if (plan_with_flags(*desc, p, false, false) != SCAN2D_OK) return 0;
   return ws_layout(*desc, p, op).total;
 }
 
 size_t scan2d_residual_bytes(const scan2d_desc* desc) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
   Plan p;
-  if (make_plan(*desc, p) != SCAN2D_OK) return 0;
+  if (plan_with_flags(*desc, p, false, false) != SCAN2D_OK) return 0;
   return res_layout(*desc, p).total;
 }
 
@@ -409,6 +457,10 @@ int scan2d_plan_info(const scan2d_desc* desc, int op, int64_t* out8) {
   if (out8 == nullptr) return SCAN2D_EINVAL;
   Plan p;
   rc = make_plan(*desc, p);
+  if (rc != SCAN2D_OK) return rc;
+  bool xvec = true, bvec = true, yvec = true;
+  vec_flags(*desc, p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, xvec, bvec, yvec);
+  rc = plan_with_flags(*desc, p, xvec, bvec);
   if (rc != SCAN2D_OK) return rc;
   const s2d::Geo& g = op == SCAN2D_OP_BWD ? p.b : p.f;
   out8[0] = g.spl * 100 + g.lpc;  // states per lane * 100 + lanes per chunk

@@ -112,21 +112,6 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
   }
 }
 
-// Warp-cooperative copy of `count` contiguous elements into 16-byte aligned
-// shared memory: 16-byte LDGSTS where the source allows, element copies for
-// the rest.
-template <typename T>
-__device__ __forceinline__ void copy_span(T* dst, const T* src, int count, int lane) {
-  constexpr int EPV = 16 / sizeof(T);
-  int done = 0;
-  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-    const int nv = count / EPV;
-    for (int u = lane; u < nv; u += 32) cp_async16(dst + u * EPV, src + u * EPV);
-    done = nv * EPV;
-  }
-  for (int u = done + lane; u < count; u += 32) cp_async_elem(dst + u, src + u);
-}
-
 // ------------------------------------------------------ gpu-scope carries
 //
 // Tags are unique per (launch, row): the host advances `epoch` by H + 1 per
@@ -156,7 +141,7 @@ struct CarrySlot<float> {
     uint64_t w;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(&p->w) : "memory");
     while (static_cast<int>(w >> 32) != tag) {
-      __nanosleep(20);
+      __nanosleep(64);
       asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(&p->w) : "memory");
     }
     return __uint_as_float(static_cast<uint32_t>(w));
@@ -189,6 +174,60 @@ struct CarrySlot<double> {
   }
   static __device__ __forceinline__ double get(const CarrySlot* p) { return p->v; }
 };
+
+// SPL consecutive carry slots (states q*SPL .. q*SPL+SPL-1 of one row).
+template <typename T, int SPL>
+__device__ __forceinline__ void carry_put(CarrySlot<T>* p, const T (&v)[SPL], int tag, int nvalid) {
+  if constexpr (sizeof(T) == 4 && SPL >= 2) {
+    if (nvalid >= SPL && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int e = 0; e < SPL; e += 2) {
+        const uint64_t w0 = (static_cast<uint64_t>(static_cast<uint32_t>(tag)) << 32) | __float_as_uint(v[e]);
+        const uint64_t w1 = (static_cast<uint64_t>(static_cast<uint32_t>(tag)) << 32) | __float_as_uint(v[e + 1]);
+        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(&p[e].w), "l"(w0), "l"(w1)
+                     : "memory");
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < SPL; ++e)
+    if (e < nvalid) CarrySlot<T>::put(p + e, v[e], tag);
+}
+
+template <typename T, int SPL>
+__device__ __forceinline__ void carry_get_wait(const CarrySlot<T>* p, T (&v)[SPL], int tag, int nvalid) {
+  if constexpr (sizeof(T) == 4 && SPL >= 2) {
+    if (nvalid >= SPL && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      uint64_t w[SPL];
+      bool ok;
+      int spins = 0;
+      do {
+        if (spins++) __nanosleep(64);
+#pragma unroll
+        for (int e = 0; e < SPL; e += 2)
+          asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                       : "=l"(w[e]), "=l"(w[e + 1])
+                       : "l"(&p[e].w)
+                       : "memory");
+        ok = true;
+#pragma unroll
+        for (int e = 0; e < SPL; ++e) ok = ok && static_cast<int>(w[e] >> 32) == tag;
+      } while (!ok);
+#pragma unroll
+      for (int e = 0; e < SPL; ++e) v[e] = __uint_as_float(static_cast<uint32_t>(w[e]));
+      return;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < SPL; ++e) v[e] = e < nvalid ? CarrySlot<T>::get_wait(p + e, tag) : T(0);
+}
+
+template <typename T, int SPL>
+__device__ __forceinline__ void carry_get(const CarrySlot<T>* p, T (&v)[SPL], int nvalid) {
+#pragma unroll
+  for (int e = 0; e < SPL; ++e) v[e] = e < nvalid ? CarrySlot<T>::get(p + e) : T(0);
+}
 
 // ------------------------------------------------------- warp collectives
 
@@ -298,6 +337,7 @@ __device__ __forceinline__ void stg_states(T* p, const T (&v)[SPL], int nvalid, 
 // J consecutive columns per lane, LPC lanes per chunk, CPW = 32/LPC chunks.
 struct Geo {
   int spl, lpc, cpw, J;
+  int Np;       // states padded to spl * lpc (zero-filled in shared memory)
   int seg;      // scans packed per warp (power of two)
   int cps;      // chunks per segment = cpw / seg
   int colsw;    // columns per warp (per segment)
@@ -305,6 +345,7 @@ struct Geo {
   int stages;   // depth of the cp.async row pipeline
   int64_t units;  // warps (= CTAs) in the launch
   int stage_elems;  // elements per pipeline stage
+  int table_off;    // element offset of the copy table in shared memory
   int smem_bytes;   // dynamic shared memory per CTA
 };
 
@@ -343,6 +384,7 @@ struct Args {
   CarrySlot<T>* rcarry;  // reverse carry at backward warp boundaries, [S][wreal_b-1][H][N]
   int* ticket;           // warp ticket counter (zeroed before each chained launch)
   uint32_t epoch;        // tag base of this launch (see row_tag)
+  int xvec, bvec, yvec;  // 16-byte copy units legal for x-like / B-like spans; vector y stores
   // shape
   int64_t S;
   int H, W, N, T_tile, P, G;

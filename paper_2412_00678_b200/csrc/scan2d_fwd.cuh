@@ -12,8 +12,8 @@
 //    of its columns lives in registers for the whole scan: no vertical
 //    carries, no look-back, no state ever written to HBM.
 //  * Row data (x, z, B, C slices) streams through a per-warp shared-memory
-//    ring of `stages` rows filled with cp.async (LDGSTS), so several rows are
-//    in flight per warp without holding registers.
+//    ring of `stages` rows filled with cp.async (scan2d_stage.cuh), so several
+//    rows are in flight per warp without holding registers.
 //  * Lanes = (chunk, state group): a lane owns SPL states (float4 loads) of J
 //    consecutive columns.  Per row it discretises its cells (softplus once per
 //    cell, spread over the chunk's lanes and shuffled), folds the J cells into
@@ -32,33 +32,45 @@
 //    every Q-column boundary) consumed by the backward kernel.
 #pragma once
 
-#include "scan2d_common.cuh"
+#include "scan2d_stage.cuh"
 
 namespace s2d {
 
-// element offsets of one pipeline stage (per segment): X | Z | [DY] | B | C
-template <typename T>
-struct StageLayout {
-  int xo, zo, dyo, bo, co, seg_stride;
-  __host__ __device__ static int pad(int n) {
-    const int e = 16 / static_cast<int>(sizeof(T));
-    return (n + e - 1) / e * e;
-  }
-  __host__ __device__ StageLayout(int colsw, int N, bool with_dy) {
-    const int pc = pad(colsw), pb = pad(colsw * N);
-    xo = 0;
-    zo = pc;
-    dyo = 2 * pc;
-    bo = (with_dy ? 3 : 2) * pc;
-    co = bo + pb;
-    seg_stride = co + pb;
-  }
-  // elements per stage incl. a tail pad for over-reading vector loads
-  __host__ __device__ static int stage_elems(int colsw, int N, int seg, bool with_dy) {
-    StageLayout L(colsw, N, with_dy);
-    return L.seg_stride * seg + pad(8);
-  }
+// Lane geometry shared by the forward and backward kernels.
+struct LaneMap {
+  int q, c, segw, lane_in_seg, gseg, cis;
+  int64_t s;    // scan of this lane
+  int64_t s0;   // first scan of the warp
+  int wpos, c0, colc, seg_scans, ncols;
+  bool scan_ok;
 };
+
+template <int LPC, int J>
+__device__ __forceinline__ LaneMap lane_map(const Geo& ge, int64_t unit, int lane, int64_t S, int W) {
+  LaneMap m;
+  m.q = lane % LPC;
+  m.c = lane / LPC;
+  m.segw = 32 / ge.seg;
+  m.lane_in_seg = lane & (m.segw - 1);
+  m.gseg = m.c / ge.cps;
+  m.cis = m.c % ge.cps;
+  if (ge.seg > 1) {
+    m.s0 = unit * ge.seg;
+    m.s = m.s0 + m.gseg;
+    m.wpos = 0;
+  } else {
+    m.s0 = unit / ge.wreal;
+    m.s = m.s0;
+    m.wpos = static_cast<int>(unit % ge.wreal);
+  }
+  m.scan_ok = m.s < S;
+  m.c0 = m.wpos * ge.colsw;
+  m.colc = m.c0 + m.cis * J;
+  const int64_t left = S - m.s0;
+  m.seg_scans = static_cast<int>(left < ge.seg ? left : ge.seg);
+  m.ncols = min(ge.colsw, W - m.c0);
+  return m;
+}
 
 template <typename T, int SPL, int LPC, int J>
 __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
@@ -68,7 +80,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
   T* smem = reinterpret_cast<T*>(smem_raw);
   const Geo& ge = a.plan.f;
   const int lane = threadIdx.x;
-  const int H = a.H, W = a.W, N = a.N;
+  const int H = a.H, W = a.W, N = a.N, Np = ge.Np;
 
   int64_t unit = blockIdx.x;
   if (ge.wreal > 1) {
@@ -76,87 +88,56 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
     if (lane == 0) t = atomicAdd(a.ticket, 1);
     unit = __shfl_sync(kFull, t, 0);
   }
-  const int q = lane % LPC;
-  const int c = lane / LPC;
-  const int segw = 32 / ge.seg;
-  const int lane_in_seg = lane & (segw - 1);
-  const int gseg = c / ge.cps;
-  const int cis = c % ge.cps;
-  int64_t s;
-  int wpos;
-  if (ge.seg > 1) {
-    s = unit * ge.seg + gseg;
-    wpos = 0;
-  } else {
-    s = unit / ge.wreal;
-    wpos = static_cast<int>(unit % ge.wreal);
-  }
-  const bool scan_ok = s < a.S;
-  const int64_t sc = scan_ok ? s : 0;
-  const int c0 = wpos * ge.colsw;
-  const int colc = c0 + cis * J;  // first column of this lane's chunk
+  const LaneMap lm = lane_map<LPC, J>(ge, unit, lane, a.S, W);
+  const int q = lm.q, cis = lm.cis, segw = lm.segw, lane_in_seg = lm.lane_in_seg;
+  const int64_t sc = lm.scan_ok ? lm.s : 0;
   const int p = static_cast<int>(sc % a.P);
-  const int64_t grp = sc / a.G;
   const size_t HW = static_cast<size_t>(H) * W;
-  const bool vec = (N % SPL) == 0;
+  const int nvalid = N - q * SPL;  // valid states of this lane's group (may be <= 0)
 
   T A2[SPL];
-  bool dok[SPL];
 #pragma unroll
   for (int e = 0; e < SPL; ++e) {
     const int d = q * SPL + e;
-    dok[e] = scan_ok && d < N;
-    A2[e] = dok[e] ? Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + d]) : T(0);
+    A2[e] = (lm.scan_ok && d < N) ? Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + d]) : T(0);
   }
   const T Dsk = a.Dskip[p], bias = a.bias[p];
 
-  // zero the ring once (no NaN garbage in never-written padding)
+  // ring + copy table
   for (int e = lane; e < ge.stages * ge.stage_elems; e += 32) smem[e] = T(0);
-  __syncwarp();
-
-  const StageLayout<T> Ls(ge.colsw, N, false);
+  const StageLayout<T> Ls(ge.colsw, Np, false);
+  Stager<T> stg;
+  stg.xvec = a.xvec != 0;
+  stg.bvec = a.bvec != 0;
+  stg.zoff = Ls.zo - Ls.xo;
+  stg.dyoff = 0;
+  stg.coff = Ls.co - Ls.bo;
+  stg.x0 = a.x + lm.s0 * HW;
+  stg.z0 = a.z + lm.s0 * HW;
+  stg.dy0 = nullptr;
+  stg.B0 = a.B + (lm.s0 / a.G) * HW * N;
+  stg.C0 = a.C + (lm.s0 / a.G) * HW * N;
+  stg.xstride = W;
+  stg.bstride = static_cast<size_t>(W) * N;
+  stg.build(reinterpret_cast<CopyEntry*>(smem + ge.table_off), lane, lm.seg_scans, lm.c0, lm.ncols, N, Np,
+            HW, Ls, lm.s0, a.G);
   const int nstage = ge.stages;
 
-  auto issue = [&](int r, int st) {
-    T* dst0 = smem + static_cast<size_t>(st) * ge.stage_elems;
-    for (int g = 0; g < ge.seg; ++g) {
-      const int64_t sg = ge.seg > 1 ? unit * ge.seg + g : s;
-      if (sg >= a.S) break;
-      const int ncols = min(ge.colsw, W - c0);
-      if (ncols <= 0) break;
-      T* dst = dst0 + g * Ls.seg_stride;
-      const size_t ro = (static_cast<size_t>(sg) * H + r) * W + c0;
-      copy_span(dst + Ls.xo, a.x + ro, ncols, lane);
-      copy_span(dst + Ls.zo, a.z + ro, ncols, lane);
-      const size_t bo = ((static_cast<size_t>(sg / a.G) * H + r) * W + c0) * N;
-      copy_span(dst + Ls.bo, a.B + bo, ncols * N, lane);
-      copy_span(dst + Ls.co, a.C + bo, ncols * N, lane);
-    }
-  };
-
-  // optional emissions (per-column tile geometry computed once)
+  // optional emissions
   const bool save = a.ckpt != nullptr;
   const bool emit_ref = a.ph != nullptr;
   const int Tt = a.T_tile;
-  const int kh = (H + Tt - 1) / Tt, kw = (W + Tt - 1) / Tt;
   const int nbm1 = a.plan.nb - 1, K = a.plan.K, Q = a.plan.Q, nq = a.plan.nq;
-  unsigned last_col_mask = 0;
-  int iwk[J], cck[J];
-#pragma unroll
-  for (int k = 0; k < J; ++k) {
-    const int j = colc + k;
-    iwk[k] = j / Tt;
-    cck[k] = j % Tt;
-    if (j < W && (cck[k] == Tt - 1 || j == W - 1)) last_col_mask |= 1u << k;
-  }
   // horizontal carry plumbing (tagged words, [S][nq][H][N])
-  const bool has_pred = wpos > 0;
-  const bool has_succ = wpos + 1 < ge.wreal;
-  CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((sc * nq + (c0 / Q - 1)) * H) * N : nullptr;
-  CarrySlot<T>* hc_out = has_succ ? a.hcarry + ((sc * nq + ((c0 + ge.colsw) / Q - 1)) * H) * N : nullptr;
-  // chunk starts on an interior Q boundary: saved for the backward
-  const bool chunk_q = save && cis > 0 && (colc % Q) == 0 && colc < W;
-  CarrySlot<T>* hc_mid = chunk_q ? a.hcarry + ((sc * nq + (colc / Q - 1)) * H) * N : nullptr;
+  const bool has_pred = lm.wpos > 0;
+  const bool has_succ = lm.wpos + 1 < ge.wreal;
+  CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((sc * nq + (lm.c0 / Q - 1)) * H) * N + q * SPL : nullptr;
+  CarrySlot<T>* hc_out =
+      has_succ ? a.hcarry + ((sc * nq + ((lm.c0 + ge.colsw) / Q - 1)) * H) * N + q * SPL : nullptr;
+  // chunk starting on an interior Q boundary: its carry-in is saved for the backward
+  const bool chunk_q = save && cis > 0 && (lm.colc % Q) == 0 && lm.colc < W;
+  CarrySlot<T>* hc_mid = chunk_q ? a.hcarry + ((sc * nq + (lm.colc / Q - 1)) * H) * N + q * SPL : nullptr;
+  T* yrow = a.y + sc * HW;
 
   T hv[J][SPL];
 #pragma unroll
@@ -164,31 +145,32 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
 #pragma unroll
     for (int e = 0; e < SPL; ++e) hv[k][e] = T(0);
 
+  __syncwarp();
   for (int r = 0; r < nstage - 1; ++r) {
-    if (r < H) issue(r, r);
+    if (r < H) stg.issue(smem + r * ge.stage_elems, r, lane, false, true);
     cp_async_commit();
   }
   int st = 0;
-  int ti = 0, ih = 0;   // row within tile / tile row (reference CarryState)
-  int kb = 0, bi = 0;   // row within band / band index (residual checkpoints)
+  int ti = 0, ih = 0;  // row within tile / tile row (reference CarryState)
+  int kb = 0, bi = 0;  // row within band / band index (residual checkpoints)
   for (int i = 0; i < H; ++i) {
     {
       const int r = i + nstage - 1;
       int sn = st + nstage - 1;
       if (sn >= nstage) sn -= nstage;
-      if (r < H) issue(r, sn);
+      if (r < H) stg.issue(smem + sn * ge.stage_elems, r, lane, false, true);
       cp_async_commit();
     }
     cp_async_wait_dyn(nstage - 1);
     __syncwarp();
-    const T* stg = smem + static_cast<size_t>(st) * ge.stage_elems + gseg * Ls.seg_stride;
+    const T* sx = smem + st * ge.stage_elems + lm.gseg * Ls.seg_stride;
 
-    // ---- discretise (math.hpp:76-89)
+    // ---- discretise (math.hpp:76-89): softplus once per cell, then shuffles
     T dl[DPL];
 #pragma unroll
     for (int m = 0; m < DPL; ++m) {
       const int kk = q + m * LPC;
-      dl[m] = kk < J ? Num<T>::softplus(stg[Ls.zo + cis * J + kk] + bias) : T(0);
+      dl[m] = kk < J ? Num<T>::softplus(sx[Ls.zo + cis * J + kk] + bias) : T(0);
     }
     T delta[J];
     const int base_lane = lane & ~(LPC - 1);
@@ -200,15 +182,14 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
 #pragma unroll
     for (int k = 0; k < J; ++k) {
       const int col = cis * J + k;
-      const bool okc = scan_ok && (c0 + col) < W;
-      const T xk = stg[Ls.xo + col];
+      const T xk = sx[Ls.xo + col];
       T bq[SPL];
-      lds_states<T, SPL>(bq, stg + Ls.bo + col * N + q * SPL, vec);
+      lds_states<T, SPL>(bq, sx + Ls.bo + col * Np + q * SPL, true);
+      const T dx = delta[k];
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
-        const bool ok = okc && dok[e];
-        av[k][e] = ok ? Num<T>::exp_scaled(delta[k] * A2[e]) : T(1);
-        uv[k][e] = ok ? (delta[k] * bq[e]) * xk : T(0);
+        av[k][e] = Num<T>::exp_scaled(dx * A2[e]);
+        uv[k][e] = (dx * bq[e]) * xk;
         if (k == 0) {
           Pc[e] = av[k][e];
           Lc[e] = uv[k][e];
@@ -249,12 +230,9 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
         }
         ew[e] = T(0);
       }
+      const int tag = row_tag(a.epoch, i);
       // ---- carry from the column group on the left
-      if (has_pred) {
-#pragma unroll
-        for (int e = 0; e < SPL; ++e)
-          if (dok[e]) ew[e] = CarrySlot<T>::get_wait(hc_in + static_cast<size_t>(i) * N + q * SPL + e, row_tag(a.epoch, i));
-      }
+      if (has_pred) carry_get_wait<T, SPL>(hc_in + static_cast<size_t>(i) * N, ew, tag, nvalid);
       if (has_succ) {
         T out[SPL];
 #pragma unroll
@@ -263,66 +241,79 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
           const T Lt = __shfl_sync(kFull, Lc[e], (CPW - 1) * LPC + q);
           out[e] = fma(Pt, ew[e], Lt);
         }
-        if (c == CPW - 1) {
-#pragma unroll
-          for (int e = 0; e < SPL; ++e)
-            if (dok[e]) CarrySlot<T>::put(hc_out + static_cast<size_t>(i) * N + q * SPL + e, out[e], row_tag(a.epoch, i));
-        }
+        if (lm.c == CPW - 1) carry_put<T, SPL>(hc_out + static_cast<size_t>(i) * N, out, tag, nvalid);
       }
 #pragma unroll
       for (int e = 0; e < SPL; ++e) hh[e] = fma(Pe[e], ew[e], Le[e]);
-      if (chunk_q) {
-#pragma unroll
-        for (int e = 0; e < SPL; ++e)
-          if (dok[e]) CarrySlot<T>::put(hc_mid + static_cast<size_t>(i) * N + q * SPL + e, hh[e], row_tag(a.epoch, i));
-      }
+      if (chunk_q) carry_put<T, SPL>(hc_mid + static_cast<size_t>(i) * N, hh, tag, nvalid);
     }
 
     // ---- horizontal then vertical recurrence, C readout
-    const bool pv_row = emit_ref && (ti == Tt - 1 || i == H - 1);
-    const bool ck_row = save && kb == K - 1 && i < H - 1;
     T yk[J];
 #pragma unroll
     for (int k = 0; k < J; ++k) {
       const int col = cis * J + k;
       T cq[SPL];
-      lds_states<T, SPL>(cq, stg + Ls.co + col * N + q * SPL, vec);
+      lds_states<T, SPL>(cq, sx + Ls.co + col * Np + q * SPL, true);
       T acc = T(0);
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
         hh[e] = fma(av[k][e], hh[e], uv[k][e]);
         const T h = fma(av[k][e], hv[k][e], hh[e]);
         hv[k][e] = h;
-        acc = fma(dok[e] ? cq[e] : T(0), h, acc);
+        acc = fma(cq[e], h, acc);
       }
       yk[k] = acc;
-      const int j = colc + k;
-      if (emit_ref && scan_ok && j < W) {
-        const size_t tile0 = (static_cast<size_t>(sc) * kh + ih) * kw + iwk[k];
-        if ((last_col_mask >> k) & 1u) {
+      if (emit_ref) {  // reference CarryState (engine.cpp:188-194, :217-220)
+        const int j = lm.colc + k;
+        if (lm.scan_ok && j < W) {
+          const int kh = (H + Tt - 1) / Tt, kw = (W + Tt - 1) / Tt;
+          const size_t tile0 = (static_cast<size_t>(sc) * kh + ih) * kw + j / Tt;
+          if (j % Tt == Tt - 1 || j == W - 1) {
 #pragma unroll
-          for (int e = 0; e < SPL; ++e)
-            if (dok[e]) a.ph[(tile0 * Tt + ti) * N + q * SPL + e] = hh[e];
-        }
-        if (pv_row) {
+            for (int e = 0; e < SPL; ++e)
+              if (e < nvalid) a.ph[(tile0 * Tt + ti) * N + q * SPL + e] = hh[e];
+          }
+          if (ti == Tt - 1 || i == H - 1) {
 #pragma unroll
-          for (int e = 0; e < SPL; ++e)
-            if (dok[e]) a.pv[(tile0 * Tt + cck[k]) * N + q * SPL + e] = hv[k][e];
+            for (int e = 0; e < SPL; ++e)
+              if (e < nvalid) a.pv[(tile0 * Tt + j % Tt) * N + q * SPL + e] = hv[k][e];
+          }
         }
       }
-      if (ck_row && scan_ok && j < W && q * SPL < N)
-        stg_states<T, SPL>(a.ckpt + ((static_cast<size_t>(sc) * nbm1 + bi) * W + j) * N + q * SPL, hv[k],
-                           N - q * SPL, vec);
+    }
+    if (save && kb == K - 1 && i < H - 1 && lm.scan_ok && nvalid > 0) {
+      T* ck = a.ckpt + ((static_cast<size_t>(sc) * nbm1 + bi) * W) * N + q * SPL;
+#pragma unroll
+      for (int k = 0; k < J; ++k) {
+        const int j = lm.colc + k;
+        if (j < W)
+          stg_states<T, SPL>(ck + static_cast<size_t>(j) * N, hv[k], nvalid, nvalid >= SPL && (N % SPL) == 0);
+      }
     }
     using RS_ = RS<LPC, J>;
     const int cbase = reduce_scatter<LPC, J>(yk, q);
-    if ((q & (RS_::kReplica - 1)) == 0 && scan_ok) {
-      T* yrow = a.y + sc * HW + static_cast<size_t>(i) * W;
+    if ((q & (RS_::kReplica - 1)) == 0 && lm.scan_ok) {
+      T* yr = yrow + static_cast<size_t>(i) * W + lm.colc + cbase;
+      const T* xr = sx + Ls.xo + cis * J + cbase;
+      if constexpr (RS_::kKeep >= 4 && sizeof(T) == 4) {
+        if (a.yvec && lm.colc + cbase + RS_::kKeep <= W) {
 #pragma unroll
-      for (int m = 0; m < RS_::kKeep; ++m) {
-        const int k = cbase + m;
-        const int j = colc + k;
-        if (j < W) yrow[j] = fma(Dsk, stg[Ls.xo + cis * J + k], yk[m]);
+          for (int m = 0; m < RS_::kKeep; m += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(xr + m);
+            *reinterpret_cast<float4*>(yr + m) =
+                make_float4(fmaf(Dsk, xv.x, yk[m]), fmaf(Dsk, xv.y, yk[m + 1]), fmaf(Dsk, xv.z, yk[m + 2]),
+                            fmaf(Dsk, xv.w, yk[m + 3]));
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < RS_::kKeep; ++m)
+            if (lm.colc + cbase + m < W) yr[m] = fma(Dsk, xr[m], yk[m]);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < RS_::kKeep; ++m)
+          if (lm.colc + cbase + m < W) yr[m] = fma(Dsk, xr[m], yk[m]);
       }
     }
     __syncwarp();

@@ -5,7 +5,7 @@
 
 #include <cuda_runtime.h>
 
-#include "scan2d_common.cuh"
+#include "scan2d_stage.cuh"
 
 namespace s2d {
 
@@ -22,7 +22,7 @@ cudaError_t launch_reduce_group(const T* per_scan, int64_t groups, int G, size_t
                                 cudaStream_t stream);
 // shared-memory geometry (elements of T)
 template <typename T>
-int stage_elems(int colsw, int N, int seg, bool bwd);
+int stage_elems(int colsw, int Np, int seg, bool bwd);
 template <typename T>
 int band_elems(int K, int J, int SPL);
 
