@@ -129,6 +129,21 @@ int scan2d_bwd_f64(const scan2d_desc* desc, const double* x, const double* z, co
                    double* dB, double* dC, double* dDskip, double* dbias, void* workspace,
                    size_t workspace_bytes, scan2d_stream_t stream);
 
+/* ---- comparator operators (Table 3 of the paper) ----
+ * SCAN2D_VARIANT_NAIVE   replaces scan2d::naive_scan_2d          (engine.hpp:108-112,
+ *                        engine.cpp:412-487): N horizontal state maps in HBM,
+ *                        then a column pass.
+ * SCAN2D_VARIANT_FLAT1D  replaces scan2d::block_scan_1d_forward  (engine.hpp:114-118,
+ *                        engine.cpp:489-526): 1D scan of the row-major flattened grid.
+ * Forward only (the reference has no backward for them). */
+#define SCAN2D_VARIANT_NAIVE 1
+#define SCAN2D_VARIANT_FLAT1D 2
+size_t scan2d_comparator_workspace_bytes(const scan2d_desc* desc, int variant);
+int scan2d_forward_variant(const scan2d_desc* desc, int variant, const void* x, const void* z,
+                           const void* B, const void* C, const void* A, const void* Dskip,
+                           const void* bias, void* y, void* workspace, size_t workspace_bytes,
+                           scan2d_stream_t stream);
+
 /* Launch geometry the library picks for a descriptor (diagnostics / bench):
  * out[0..7] = {lanes_per_chunk, cols_per_chunk, scans_per_warp, warps_per_scan,
  *              warps_per_cta, ctas_per_scan_row, total_ctas, band_rows}. */

@@ -283,7 +283,7 @@ static inline float abar_f32(float delta, float a) { return orc_fast_expf(delta 
         }                                                                                \
         dx[cell] = FMA(D, dyv, dv * sum_ghor_b);                                         \
         dz[cell] = ddelta * sig;                                                         \
-        dbias_t = FMA(ddelta, sig, dbias_t); /* contracted += (engine.cpp:394) */        \
+        dbias_t += ddelta * sig; /* product shared with dz: not contracted (:393-394) */   \
         dd_t = FMA(dyv, xv, dd_t);           /* contracted += (engine.cpp:395) */        \
       }                                                                                  \
     *dD = dd_t;                                                                          \

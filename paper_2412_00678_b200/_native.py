@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libscan2d_cuda.so")
 OK, EINVAL, ESTALE, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4, 5
 F32, F64 = 0, 1
 OP_FWD, OP_BWD = 0, 1
+VARIANT_NAIVE, VARIANT_FLAT1D = 1, 2
 MAX_STATE_DIM = 2048
 
 # every symbol include/scan2d_cuda.h declares
@@ -29,6 +30,8 @@ EXPORTED_SYMBOLS = (
     "scan2d_bwd_f32",
     "scan2d_bwd_f64",
     "scan2d_plan_info",
+    "scan2d_comparator_workspace_bytes",
+    "scan2d_forward_variant",
     "scan2d_last_launch_count",
     "scan2d_status_string",
     "scan2d_version",
@@ -81,6 +84,10 @@ def _load():
     for name in ("scan2d_bwd_f32", "scan2d_bwd_f64"):
         getattr(lib, name).argtypes = [D] + [P] * 17 + [C.c_size_t, P]
         getattr(lib, name).restype = C.c_int
+    lib.scan2d_comparator_workspace_bytes.argtypes = [D, C.c_int]
+    lib.scan2d_comparator_workspace_bytes.restype = C.c_size_t
+    lib.scan2d_forward_variant.argtypes = [D, C.c_int] + [P] * 9 + [C.c_size_t, P]
+    lib.scan2d_forward_variant.restype = C.c_int
     lib.scan2d_plan_info.argtypes = [D, C.c_int, C.POINTER(C.c_int64)]
     lib.scan2d_plan_info.restype = C.c_int
     lib.scan2d_last_launch_count.argtypes = []

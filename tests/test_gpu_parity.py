@@ -273,3 +273,119 @@ def test_closed_form_large_grid(s2d):
     geo = lambda k: (1 - a_target ** (k + 1)) / (1 - a_target)
     expect = 0.5 * geo(i) * geo(j)
     assert rel_error(y, expect) <= 1e-12
+
+
+# ------------------------------------------------- reference golden vectors
+
+GOLDEN = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)),
+                                    "golden", "reference_golden.npz")
+FWD_GOLD = [(11, 7, 4, (64,), 42), (6, 9, 3, (1,), 43), (8, 8, 2, (3,), 44), (13, 10, 5, (1, 2, 3, 8, 13), 45),
+            (33, 29, 6, (8,), 48), (23, 17, 3, (8,), 1000 + 23 * 31 + 17)]
+BWD_GOLD = [(5, 6, 3, 2, 60), (7, 4, 2, 3, 62), (5, 4, 3, 3, 0), (4, 5, 2, 6, 7), (17, 13, 4, 4, 63),
+            (16, 16, 16, 16, 1000)]
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_forward_vs_reference_golden(orc, s2d, dt):
+    """y and the CarryState against numbers produced by the reference library itself."""
+    gold = np.load(GOLDEN)
+    gate = F64_Y_GATE if dt == "f64" else 1e-5
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    for h, w, n, tiles, seed in FWD_GOLD:
+        key = f"fwd_{h}x{w}_n{n}_s{seed}_{dt}"
+        b = make_batch(orc, 1, h, w, n, seed0=seed, dtype=dt)
+        assert np.array_equal(b.x.ravel(), gold[key + "_x"])
+        for t in tiles:
+            res, _ = run_fwd(s2d, b, tdt, tile=t, carries=True)
+            assert rel_error(res.y.cpu().numpy(), gold[f"{key}_t{t}_y"]) <= gate, (key, t)
+            assert rel_error(res.ph.cpu().numpy(), gold[f"{key}_t{t}_ph"]) <= gate, (key, t)
+            assert rel_error(res.pv.cpu().numpy(), gold[f"{key}_t{t}_pv"]) <= gate, (key, t)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_backward_vs_reference_golden(orc, s2d, dt):
+    gold = np.load(GOLDEN)
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    for h, w, n, t, seed in BWD_GOLD:
+        key = f"bwd_{h}x{w}_n{n}_s{seed}_t{t}_{dt}"
+        b = make_batch(orc, 1, h, w, n, seed0=seed, dtype=dt)
+        res, dy = run_fwd(s2d, b, tdt, tile=t)
+        g = grads_np(s2d.tiled_scan_2d_backward(res.saved, dy))
+        for k in ("dx", "dz", "dA", "dB", "dC", "dD", "dbias"):
+            e = rel_error(g[k], gold[f"{key}_{k}"])
+            assert e <= (F64_G_GATE if dt == "f64" else F32_GATE), (key, k, e)
+
+
+def test_config1_vs_reference_golden(orc, s2d):
+    """BASELINE.json configs[0] (64 scans, 16x16, N=16, fp32): the batched GPU
+    forward against the reference engine's outputs, scan by scan."""
+    gold = np.load(GOLDEN)["cfg1_y_f32"]
+    b = make_batch(orc, 64, 16, 16, 16, seed0=1000, dtype="f32")
+    res, _ = run_fwd(s2d, b, torch.float32)
+    y = res.y.cpu().numpy().reshape(64, -1)
+    for s in range(64):
+        assert rel_error(y[s], gold[s]) <= 1e-5
+
+
+def test_reference_suite_against_cuda_engine():
+    """The reference's own doctest suites (engine, backward, memsim, reference,
+    block_scan) linked against the CUDA engine shim instead of engine.cpp."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "ref_tests_cuda")
+    if not os.path.exists(exe):
+        pytest.skip("ref_tests_cuda not built (needs the reference sources at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert " 0 failed" in r.stdout
+
+
+# ------------------------------------------------------------- comparators
+
+
+def _variant(s2d, b, variant, dtype):
+    import ctypes as C
+
+    from paper_2412_00678_b200 import _native as nat
+
+    (x, z, B, Cc, A, D, bias), _ = batch_to_torch(b, dtype=dtype)
+    desc = nat.make_desc(b.S, b.H, b.W, b.N, params_period=b.P, bc_group=b.G,
+                         dtype=nat.F64 if dtype == torch.float64 else nat.F32)
+    y = torch.empty_like(x)
+    wsb = nat.lib.scan2d_comparator_workspace_bytes(C.byref(desc), variant)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=x.device)
+    p = lambda t: C.c_void_p(t.data_ptr())
+    rc = nat.lib.scan2d_forward_variant(C.byref(desc), variant, p(x), p(z), p(B), p(Cc), p(A), p(D), p(bias), p(y),
+                                        p(ws), wsb, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == nat.OK
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def test_naive_comparator_vs_oracle(orc, s2d):
+    from paper_2412_00678_b200 import _native as nat
+
+    b = make_batch(orc, 3, 13, 17, 5, seed0=71, dtype="f64")
+    assert rel_error(_variant(s2d, b, nat.VARIANT_NAIVE, torch.float64), oracle_fwd(orc, b, "f64")) <= F64_Y_GATE
+
+
+def test_flat1d_comparator_vs_sequential(orc, s2d):
+    """block_scan_1d_forward == scan_1d_sequential on the row-major flattening
+    (test_engine.cpp:75-82)."""
+    from paper_2412_00678_b200 import _native as nat
+
+    b = make_batch(orc, 2, 5, 8, 3, seed0=47, dtype="f64")
+    y = _variant(s2d, b, nat.VARIANT_FLAT1D, torch.float64)
+    for s in range(b.S):
+        L = b.H * b.W
+        x, z = b.x[s].ravel(), b.z[s].ravel()
+        B, Cc = b.B[s].reshape(L, b.N), b.C[s].reshape(L, b.N)
+        delta = np.where(z + b.bias[s] > 20, z + b.bias[s], np.log1p(np.exp(z + b.bias[s])))
+        h = np.zeros(b.N)
+        ref = np.empty(L)
+        for k in range(L):
+            h = np.exp(delta[k] * b.A[s]) * h + delta[k] * B[k] * x[k]
+            ref[k] = (Cc[k] * h).sum() + b.D[s] * x[k]
+        assert rel_error(y[s].ravel(), ref) <= 1e-12
