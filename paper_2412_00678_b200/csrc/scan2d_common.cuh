@@ -83,6 +83,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16_raw(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_elem(float* smem, const float* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem)
                : "memory");
@@ -221,6 +224,44 @@ __device__ __forceinline__ void carry_get_wait(const CarrySlot<T>* p, T (&v)[SPL
   }
 #pragma unroll
   for (int e = 0; e < SPL; ++e) v[e] = e < nvalid ? CarrySlot<T>::get_wait(p + e, tag) : T(0);
+}
+
+// Prefetchable carry read: `carry_load` issues the loads (no waiting) and
+// `carry_resolve` checks the tags, re-polling only if the producer was late.
+template <typename T, int SPL>
+struct CarryPre {
+  uint64_t w[SPL];
+};
+
+template <int SPL>
+__device__ __forceinline__ void carry_load(const CarrySlot<float>* p, CarryPre<float, SPL>& c) {
+  if constexpr (SPL >= 2) {
+#pragma unroll
+    for (int e = 0; e < SPL; e += 2)
+      asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                   : "=l"(c.w[e]), "=l"(c.w[e + 1])
+                   : "l"(&p[e].w)
+                   : "memory");
+  } else {
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(c.w[0]) : "l"(&p[0].w) : "memory");
+  }
+}
+
+template <int SPL>
+__device__ __forceinline__ void carry_resolve(const CarrySlot<float>* p, CarryPre<float, SPL>& c, int tag,
+                                              float (&v)[SPL]) {
+  bool ok = true;
+#pragma unroll
+  for (int e = 0; e < SPL; ++e) ok = ok && static_cast<int>(c.w[e] >> 32) == tag;
+  while (!ok) {
+    __nanosleep(64);
+    carry_load<SPL>(p, c);
+    ok = true;
+#pragma unroll
+    for (int e = 0; e < SPL; ++e) ok = ok && static_cast<int>(c.w[e] >> 32) == tag;
+  }
+#pragma unroll
+  for (int e = 0; e < SPL; ++e) v[e] = __uint_as_float(static_cast<uint32_t>(c.w[e]));
 }
 
 template <typename T, int SPL>

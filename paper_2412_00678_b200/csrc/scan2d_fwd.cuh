@@ -122,6 +122,20 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
   stg.build(reinterpret_cast<CopyEntry*>(smem + ge.table_off), lane, lm.seg_scans, lm.c0, lm.ncols, N, Np,
             HW, Ls, lm.s0, a.G);
   const int nstage = ge.stages;
+  // static staging: one unpacked scan per warp, 16-byte units legal
+  constexpr int EPV = 16 / static_cast<int>(sizeof(T));
+  constexpr int MX = (CPW * J + 32 * EPV - 1) / (32 * EPV);
+  constexpr int MB = (J * SPL + EPV - 1) / EPV;
+  const bool sstat = ge.seg == 1 && a.xvec && a.bvec;
+  const int xunits = lm.ncols / EPV, bunits = lm.ncols * N / EPV;
+  const uint32_t smem_addr = smem_u32(smem);
+  auto issue_row = [&](int r, int st_) {
+    if (sstat)
+      stg.template issue_static<MX, MB>(smem_addr + st_ * ge.stage_elems * static_cast<int>(sizeof(T)), r, lane,
+                                        xunits, bunits, Ls, false, true);
+    else
+      stg.issue(smem + st_ * ge.stage_elems, r, lane, false, true);
+  };
 
   // optional emissions
   const bool save = a.ckpt != nullptr;
@@ -147,7 +161,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
 
   __syncwarp();
   for (int r = 0; r < nstage - 1; ++r) {
-    if (r < H) stg.issue(smem + r * ge.stage_elems, r, lane, false, true);
+    if (r < H) issue_row(r, r);
     cp_async_commit();
   }
   int st = 0;
@@ -158,12 +172,17 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
       const int r = i + nstage - 1;
       int sn = st + nstage - 1;
       if (sn >= nstage) sn -= nstage;
-      if (r < H) stg.issue(smem + sn * ge.stage_elems, r, lane, false, true);
+      if (r < H) issue_row(r, sn);
       cp_async_commit();
     }
     cp_async_wait_dyn(nstage - 1);
     __syncwarp();
     const T* sx = smem + st * ge.stage_elems + lm.gseg * Ls.seg_stride;
+    // issue the carry-in load now; it is resolved after the row's local work
+    CarryPre<T, SPL> cpre;
+    const bool fast_carry = sizeof(T) == 4 && has_pred && nvalid >= SPL && (N % 2 == 0 || SPL == 1);
+    if (fast_carry) carry_load<SPL>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i) * N),
+                                    *reinterpret_cast<CarryPre<float, SPL>*>(&cpre));
 
     // ---- discretise (math.hpp:76-89): softplus once per cell, then shuffles
     T dl[DPL];
@@ -209,12 +228,11 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
         Pu[e] = __shfl_up_sync(kFull, Pc[e], off, segw);
         Lu[e] = __shfl_up_sync(kFull, Lc[e], off, segw);
       }
-      if (lane_in_seg >= off) {
+      const bool act = lane_in_seg >= off;
 #pragma unroll
-        for (int e = 0; e < SPL; ++e) {
-          Lc[e] = fma(Pc[e], Lu[e], Lc[e]);
-          Pc[e] = Pc[e] * Pu[e];
-        }
+      for (int e = 0; e < SPL; ++e) {
+        Lc[e] = act ? fma(Pc[e], Lu[e], Lc[e]) : Lc[e];
+        Pc[e] = act ? Pc[e] * Pu[e] : Pc[e];
       }
     }
     T hh[SPL];
@@ -232,7 +250,13 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
       }
       const int tag = row_tag(a.epoch, i);
       // ---- carry from the column group on the left
-      if (has_pred) carry_get_wait<T, SPL>(hc_in + static_cast<size_t>(i) * N, ew, tag, nvalid);
+      if (fast_carry) {
+        if constexpr (sizeof(T) == 4)
+          carry_resolve<SPL>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i) * N), cpre,
+                             tag, ew);
+      } else if (has_pred) {
+        carry_get_wait<T, SPL>(hc_in + static_cast<size_t>(i) * N, ew, tag, nvalid);
+      }
       if (has_succ) {
         T out[SPL];
 #pragma unroll

@@ -112,8 +112,38 @@ struct Stager {
     __syncwarp();
   }
 
-  // Issue the copies of row r into stage `stage` (x, z always; B, C when
-  // with_c is false only B ... see flags).
+  // Static fast path (one unpacked scan per warp, 16-byte units legal): lane
+  // copies x/z unit `lane` and B/C units lane + 32 m, m < MB = J*SPL/4, all
+  // with immediate offsets; `stage_addr` is the shared address of the stage.
+  template <int MX, int MB>
+  __device__ __forceinline__ void issue_static(uint32_t stage_addr, int r, int lane, int xunits, int bunits,
+                                               const StageLayout<T>& L, bool with_dy, bool with_c) const {
+    constexpr int es = static_cast<int>(sizeof(T));
+    const T* xs = x0 + r * xstride + lane * EPV;
+    const T* zs = z0 + r * xstride + lane * EPV;
+    const uint32_t xd = stage_addr + (L.xo + lane * EPV) * es;
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      if (lane + 32 * m < xunits) {
+        cp_async16_raw(xd + m * 512, xs + m * 32 * EPV);
+        cp_async16_raw(xd + zoff * es + m * 512, zs + m * 32 * EPV);
+        if (with_dy) cp_async16_raw(xd + dyoff * es + m * 512, dy0 + r * xstride + lane * EPV + m * 32 * EPV);
+      }
+    }
+    const T* bs = B0 + r * bstride + lane * EPV;
+    const T* cs = C0 + r * bstride + lane * EPV;
+    const uint32_t bd = stage_addr + (L.bo + lane * EPV) * es;
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      if (lane + 32 * m < bunits) {
+        cp_async16_raw(bd + m * 512, bs + m * 32 * EPV);
+        if (with_c) cp_async16_raw(bd + coff * es + m * 512, cs + m * 32 * EPV);
+      }
+    }
+  }
+
+  // Issue the copies of row r into stage `stage` (x, z always; dy / C when
+  // requested).
   __device__ __forceinline__ void issue(T* stage, int r, int lane, bool with_dy, bool with_c) const {
     const T* xr = x0 + r * xstride;
     const T* zr = z0 + r * xstride;
