@@ -70,12 +70,15 @@ struct Stager {
   const T* B0;
   const T* C0;
   size_t xstride, bstride;
+  int xc0, bc0;  // column offset of the warp's window in x-like / B-like rows (static path)
 
   // Build the lane's table (once).  seg_scans: scans present in this warp
   // (>= 1), c0 / ncols: column window, N / Np: states and padded states.
   __device__ void build(CopyEntry* table, int lane, int seg_scans, int c0, int ncols, int N, int Np,
                         size_t HW, const StageLayout<T>& L, int64_t s0, int G) {
     xt = table;
+    xc0 = c0;
+    bc0 = c0 * N;
     const int xper = xvec ? ncols / EPV : ncols;
     const int xtot = seg_scans * xper;
     nx = (xtot + 31) / 32;
@@ -119,19 +122,20 @@ struct Stager {
   __device__ __forceinline__ void issue_static(uint32_t stage_addr, int r, int lane, int xunits, int bunits,
                                                const StageLayout<T>& L, bool with_dy, bool with_c) const {
     constexpr int es = static_cast<int>(sizeof(T));
-    const T* xs = x0 + r * xstride + lane * EPV;
-    const T* zs = z0 + r * xstride + lane * EPV;
+    const T* xs = x0 + r * xstride + xc0 + lane * EPV;
+    const T* zs = z0 + r * xstride + xc0 + lane * EPV;
     const uint32_t xd = stage_addr + (L.xo + lane * EPV) * es;
 #pragma unroll
     for (int m = 0; m < MX; ++m) {
       if (lane + 32 * m < xunits) {
         cp_async16_raw(xd + m * 512, xs + m * 32 * EPV);
         cp_async16_raw(xd + zoff * es + m * 512, zs + m * 32 * EPV);
-        if (with_dy) cp_async16_raw(xd + dyoff * es + m * 512, dy0 + r * xstride + lane * EPV + m * 32 * EPV);
+        if (with_dy)
+          cp_async16_raw(xd + dyoff * es + m * 512, dy0 + r * xstride + xc0 + lane * EPV + m * 32 * EPV);
       }
     }
-    const T* bs = B0 + r * bstride + lane * EPV;
-    const T* cs = C0 + r * bstride + lane * EPV;
+    const T* bs = B0 + r * bstride + bc0 + lane * EPV;
+    const T* cs = C0 + r * bstride + bc0 + lane * EPV;
     const uint32_t bd = stage_addr + (L.bo + lane * EPV) * es;
 #pragma unroll
     for (int m = 0; m < MB; ++m) {
