@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 
@@ -48,6 +49,15 @@ int check_desc(const scan2d_desc* d) {
 
 // Geometry of one direction (see s2d::Geo).  N <= 128: SPL = 4 states per lane
 // (float4), LPC = Np / 4 lanes per chunk; N <= 2 uses SPL = Np, LPC = 1.
+// Tuning overrides (diagnostics / sweeps only): SCAN2D_FWD_J, SCAN2D_BWD_J,
+// SCAN2D_FWD_STAGES, SCAN2D_BWD_STAGES, SCAN2D_BAND_ROWS.
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  if (v == nullptr || *v == 0) return dflt;
+  const int x = std::atoi(v);
+  return x > 0 ? x : dflt;
+}
+
 s2d::Geo make_geo(const scan2d_desc& d, bool bwd) {
   s2d::Geo g{};
   const int N = d.state_dim, W = d.width;
@@ -62,6 +72,9 @@ s2d::Geo make_geo(const scan2d_desc& d, bool bwd) {
   else
     g.J = bwd ? 4 : 8;
   if (dbl) g.J = std::min(g.J, 2);
+  g.J = env_int(bwd ? "SCAN2D_BWD_J" : "SCAN2D_FWD_J", g.J);
+  if (g.J != 1 && g.J != 2 && g.J != 4 && g.J != 8) g.J = 2;
+  if (bwd && g.J > 4) g.J = 4;
   const int chunks = static_cast<int>(ceil_div(W, g.J));
   if (chunks <= g.cpw / 2) {
     g.cps = next_pow2(chunks);
@@ -73,7 +86,8 @@ s2d::Geo make_geo(const scan2d_desc& d, bool bwd) {
   g.colsw = g.cps * g.J;
   g.wreal = g.seg > 1 ? 1 : static_cast<int>(ceil_div(W, g.colsw));
   g.units = ceil_div(d.num_scans, g.seg) * g.wreal;
-  g.stages = bwd ? 3 : 4;
+  g.stages = env_int(bwd ? "SCAN2D_BWD_STAGES" : "SCAN2D_FWD_STAGES", bwd ? 3 : 4);
+  g.stages = std::max(2, std::min(8, g.stages));
   return g;
 }
 
@@ -103,7 +117,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
   p.b = make_geo(d, true);
   p.f = make_geo(d, false);
-  p.K = std::min(8, static_cast<int>(d.height));
+  p.K = std::min(env_int("SCAN2D_BAND_ROWS", 8), static_cast<int>(d.height));
   p.nb = static_cast<int>(ceil_div(d.height, p.K));
   if (p.b.wreal > 1) {
     p.Q = p.b.colsw;
