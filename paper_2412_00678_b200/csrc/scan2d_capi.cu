@@ -152,9 +152,50 @@ void vec_flags(const scan2d_desc& d, const Plan& p, const void* x, const void* z
   yvec = al(y) && (d.width % 4) == 0;
 }
 
+// Tile-transpose forward (scan2d_tile.cuh): N in {4, 8, 16, 32}, 16-byte copy
+// units legal, strips of 16 columns (the carry grid Q becomes 16).
+bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec) {
+  const int N = d.state_dim;
+  if (!(N == 4 || N == 8 || N == 16 || N == 32) || !xvec || !bvec) return false;
+  return env_int("SCAN2D_TILE_FWD", 1) == 1;
+}
+
 int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
   int rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
+  if (use_tile_fwd(d, xvec, bvec)) {
+    const bool dbl = d.dtype == SCAN2D_F64;
+    s2d::Geo& g = p.f;
+    g.tile = 1;
+    g.spl = 4;
+    g.lpc = d.state_dim / 4;
+    g.cpw = 32 / g.lpc;
+    g.J = 1;
+    g.Np = d.state_dim;
+    g.seg = 1;
+    g.cps = g.cpw;
+    g.colsw = 16;
+    g.wreal = static_cast<int>(ceil_div(d.width, 16));
+    g.units = d.num_scans * g.wreal;
+    g.stages = env_int("SCAN2D_TILE_STAGES", 2);
+    // horizontal carries on the 16-column strip grid
+    p.Q = 16;
+    p.nq = static_cast<int>(ceil_div(d.width, 16)) - 1;
+    // the backward's column groups must sit on the same grid
+    while (p.b.wreal > 1 && (p.b.colsw % 16) != 0 && p.b.J < 4) {
+      p.b.J *= 2;
+      p.b.colsw = p.b.cps * p.b.J;
+      p.b.wreal = static_cast<int>(ceil_div(d.width, p.b.colsw));
+      p.b.units = ceil_div(d.num_scans, p.b.seg) * p.b.wreal;
+    }
+    if (p.b.wreal > 1 && (p.b.colsw % 16) != 0) return SCAN2D_EUNSUPPORTED;
+    const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.stages) : s2d::tile_elems<float>(d.state_dim, g.stages);
+    g.stage_elems = 0;
+    g.table_off = 0;
+    g.smem_bytes = static_cast<int>(static_cast<size_t>(el) * dtype_size(d.dtype));
+    if (g.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
+    return finish_geo(p.b, d, true, p.K, xvec, bvec);
+  }
   rc = finish_geo(p.f, d, false, p.K, xvec, bvec);
   if (rc != SCAN2D_OK) return rc;
   return finish_geo(p.b, d, true, p.K, xvec, bvec);

@@ -25,5 +25,10 @@ template <typename T>
 int stage_elems(int colsw, int Np, int seg, bool bwd);
 template <typename T>
 int band_elems(int K, int J, int SPL);
+// tile-transpose forward: shared elements for `stages` tiles, rows per tile
+template <typename T>
+int tile_elems(int N, int stages);
+template <typename T>
+int tile_rows(int N);
 
 }  // namespace s2d

@@ -1,0 +1,272 @@
+// scan2d_tile.cuh -- "tile-transpose" forward kernel for N >= 4 (sm_100a).
+//
+// Same recurrences as scan2d_fwd.cuh (reference.cpp:85-112):
+//   hh(i,j) = fma(Abar, hh(i,j-1), Bbar x)      h(i,j) = fma(Abar, h(i-1,j), hh(i,j))
+//   y(i,j)  = D x + sum_d C h
+// but organised so that neither scan needs shuffles:
+//  * one warp owns a STRIP of CW columns of one scan and walks it in tiles of
+//    R rows (R * N/4 = 32: R = 8 rows for N = 16);
+//  * phase 1 (row lanes): lane (r, q) owns row r of the tile and states
+//    4q..4q+3; it walks the CW columns left to right with the horizontal
+//    carry in registers (4 independent FMA chains) and writes hh to shared
+//    memory.  The strip's carry-in per row comes from the strip on the left
+//    (tagged words in global memory, one hop per tile);
+//  * phase 2 (column lanes): lane (j, s) owns column j and N/QV states; it
+//    walks the R rows top to bottom with the vertical state h in registers
+//    for the whole scan, reads hh back, and folds C h into y (one xor shuffle
+//    when a column is split over QV = 32/CW lanes).
+// Shared-memory rows are padded so that both the row-lane and the
+// column-lane access patterns are bank-conflict free.  Tiles stream through a
+// cp.async ring (2-3 tiles), copied with 16-byte units and immediate offsets.
+#pragma once
+
+#include "scan2d_fwd.cuh"
+
+namespace s2d {
+
+template <typename T, int N, int CW>
+struct TileShape {
+  static constexpr int QH = N / 4;            // row lanes per row (4 states each)
+  static constexpr int R = 32 / QH;           // rows per tile
+  static constexpr int QV = 32 / CW;          // column lanes per column
+  static constexpr int SV = N / QV;           // states per column lane
+  static constexpr int PAD = 4 * QH;          // row padding of the [R][CW][N] blocks (floats)
+  static constexpr int BP = CW * N + PAD;     // padded row pitch of B / C / HH
+  static constexpr int XP = CW;               // row pitch of X / Z / DL
+  // stage: X[R][XP] Z[R][XP] B[R][BP] C[R][BP]
+  static constexpr int XO = 0, ZO = R * XP, BO = 2 * R * XP, CO = BO + R * BP;
+  static constexpr int STAGE = CO + R * BP;
+  // scratch after the stages: HH[R][BP], DL[R][XP]
+  static constexpr int SCRATCH = R * BP + R * XP;
+  static constexpr int EPV = 16 / sizeof(T);
+  static constexpr int XU = R * CW / EPV;         // 16-byte units of one X (or Z) tile
+  static constexpr int BU = R * CW * N / EPV;     // 16-byte units of one B (or C) tile
+  static constexpr int XUL = (XU + 31) / 32;      // per lane
+  static constexpr int BUL = (BU + 31) / 32;
+  static constexpr int BUR = CW * N / EPV;        // units per row of B
+  static_assert(QH >= 1 && R >= 1 && QV >= 1 && SV >= 1, "bad tile shape");
+};
+
+template <typename T, int N, int CW>
+__global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a) {
+  using TS = TileShape<T, N, CW>;
+  constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, EPV = TS::EPV;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  const Geo& ge = a.plan.f;
+  const int lane = threadIdx.x;
+  const int H = a.H, W = a.W;
+  const int nstage = ge.stages;
+
+  int64_t unit = blockIdx.x;
+  if (ge.wreal > 1) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1);
+    unit = __shfl_sync(kFull, t, 0);
+  }
+  const int64_t s = unit / ge.wreal;
+  const int wpos = static_cast<int>(unit % ge.wreal);
+  const int c0 = wpos * CW;
+  const int ncols = min(CW, W - c0);
+  const int p = static_cast<int>(s % a.P);
+  const size_t HW = static_cast<size_t>(H) * W;
+  const T Dsk = a.Dskip[p], bias = a.bias[p];
+
+  // phase-1 identity: row r1, states 4*q1 .. 4*q1+3
+  const int r1 = lane / QH, q1 = lane % QH;
+  // phase-2 identity: column j2, states s2*SV .. s2*SV+SV-1
+  const int j2 = lane / QV, s2 = lane % QV;
+  T A1[4], A2v[SV];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * 4 + e]);
+#pragma unroll
+  for (int e = 0; e < SV; ++e) A2v[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
+
+  T* hhs = smem + nstage * TS::STAGE;  // [R][BP]
+  T* dls = hhs + R * TS::BP;           // [R][XP]
+  for (int e = lane; e < nstage * TS::STAGE; e += 32) smem[e] = T(0);
+  __syncwarp();
+
+  // ---- tile copies (rows r0 .. r0+R-1, columns c0 .. c0+ncols-1)
+  const T* xg = a.x + s * HW + c0;
+  const T* zg = a.z + s * HW + c0;
+  const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
+  const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
+  const int xunits_row = ncols / EPV, bunits_row = ncols * N / EPV;
+  const uint32_t sbase = smem_u32(smem);
+  auto issue_tile = [&](int r0, int st) {
+    const uint32_t sb = sbase + st * TS::STAGE * static_cast<int>(sizeof(T));
+#pragma unroll
+    for (int m = 0; m < TS::XUL; ++m) {
+      const int u = lane + 32 * m;
+      const int rr = u / (CW / EPV), cu = u % (CW / EPV);
+      if (u < TS::XU && cu < xunits_row && r0 + rr < H) {
+        const size_t go = static_cast<size_t>(r0 + rr) * W + cu * EPV;
+        const uint32_t so = (rr * TS::XP + cu * EPV) * sizeof(T);
+        cp_async16_raw(sb + (TS::XO * sizeof(T)) + so, xg + go);
+        cp_async16_raw(sb + (TS::ZO * sizeof(T)) + so, zg + go);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < TS::BUL; ++m) {
+      const int u = lane + 32 * m;
+      const int rr = u / TS::BUR, cu = u % TS::BUR;
+      if (u < TS::BU && cu < bunits_row && r0 + rr < H) {
+        const size_t go = static_cast<size_t>(r0 + rr) * W * N + cu * EPV;
+        const uint32_t so = (rr * TS::BP + cu * EPV) * sizeof(T);
+        cp_async16_raw(sb + (TS::BO * sizeof(T)) + so, Bg + go);
+        cp_async16_raw(sb + (TS::CO * sizeof(T)) + so, Cg + go);
+      }
+    }
+  };
+
+  // ---- carries (tagged words [S][nq][H][N]); strips are the Q grid (Q == CW)
+  const bool save = a.ckpt != nullptr;
+  const int nq = a.plan.nq, K = a.plan.K, nbm1 = a.plan.nb - 1;
+  const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * 4 : nullptr;
+  CarrySlot<T>* hc_out = has_succ ? a.hcarry + ((s * nq + wpos) * H) * N + q1 * 4 : nullptr;
+  const bool emit_ref = a.ph != nullptr;
+  const int Tt = a.T_tile;
+  const int kh = (H + Tt - 1) / Tt, kw = (W + Tt - 1) / Tt;
+
+  T hv[SV];
+#pragma unroll
+  for (int e = 0; e < SV; ++e) hv[e] = T(0);
+
+  const int ntiles = (H + R - 1) / R;
+  for (int t = 0; t < nstage - 1; ++t) {
+    if (t < ntiles) issue_tile(t * R, t);
+    cp_async_commit();
+  }
+  int st = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    const int r0 = t * R;
+    {
+      const int tn = t + nstage - 1;
+      int sn = st + nstage - 1;
+      if (sn >= nstage) sn -= nstage;
+      if (tn < ntiles) issue_tile(tn * R, sn);
+      cp_async_commit();
+    }
+    // carry-in for this lane's row, issued before the wait so it overlaps
+    const int i1 = r0 + r1;
+    const bool row1_ok = i1 < H;
+    CarryPre<T, 4> cpre;
+    if constexpr (sizeof(T) == 4) {
+      if (has_pred && row1_ok)
+        carry_load<4>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
+                      *reinterpret_cast<CarryPre<float, 4>*>(&cpre));
+    }
+    cp_async_wait_dyn(nstage - 1);
+    __syncwarp();
+    const T* sg = smem + st * TS::STAGE;
+
+    // ================= phase 1: horizontal scan, lane = (row r1, states 4 q1 ..)
+    // delta for the row's cells: the QH lanes of a row split its CW cells
+#pragma unroll
+    for (int m = 0; m < CW / QH; ++m) {
+      const int j = q1 + m * QH;
+      dls[r1 * TS::XP + j] = Num<T>::softplus(sg[TS::ZO + r1 * TS::XP + j] + bias);
+    }
+    __syncwarp();
+    T hh[4];
+    if (has_pred && row1_ok) {
+      if constexpr (sizeof(T) == 4) {
+        carry_resolve<4>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N), cpre,
+                         row_tag(a.epoch, i1), hh);
+      } else {
+        carry_get_wait<T, 4>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), 4);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hh[e] = T(0);
+    }
+    {
+      const T* xr = sg + TS::XO + r1 * TS::XP;
+      const T* dr = dls + r1 * TS::XP;
+      const T* br = sg + TS::BO + r1 * TS::BP + q1 * 4;
+      T* hr = hhs + r1 * TS::BP + q1 * 4;
+#pragma unroll 4
+      for (int j = 0; j < CW; ++j) {
+        T b4[4];
+        lds_states<T, 4>(b4, br + j * N, true);
+        const T dj = dr[j], xj = xr[j];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const T av = Num<T>::exp_scaled(dj * A1[e]);
+          hh[e] = fma(av, hh[e], (dj * b4[e]) * xj);
+        }
+        if (j < ncols) {
+          if constexpr (sizeof(T) == 4) {
+            *reinterpret_cast<float4*>(hr + j * N) = make_float4(hh[0], hh[1], hh[2], hh[3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hr[j * N + e] = hh[e];
+          }
+        }
+        if (emit_ref && row1_ok && j < ncols) {  // reference P^h (engine.cpp:186-194)
+          const int jg = c0 + j;
+          if (jg % Tt == Tt - 1 || jg == W - 1) {
+            const size_t tile0 = (static_cast<size_t>(s) * kh + i1 / Tt) * kw + jg / Tt;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) a.ph[(tile0 * Tt + i1 % Tt) * N + q1 * 4 + e] = hh[e];
+          }
+        }
+        if (j == ncols - 1 && has_succ && row1_ok)
+          carry_put<T, 4>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), 4);
+      }
+    }
+    __syncwarp();
+
+    // ================= phase 2: vertical scan + readout, lane = (column j2, states s2 SV ..)
+    {
+      const int jg = c0 + j2;
+      const bool col_ok = j2 < ncols;
+      const T* hcol = hhs + j2 * N + s2 * SV;
+      const T* ccol = sg + TS::CO + j2 * N + s2 * SV;
+      for (int r = 0; r < R; ++r) {
+        const int i = r0 + r;
+        if (i >= H) break;
+        const T dj = dls[r * TS::XP + j2];
+        T acc = T(0);
+#pragma unroll
+        for (int e0 = 0; e0 < SV; e0 += 4) {
+          T h4[4], c4[4];
+          lds_states<T, 4>(h4, hcol + r * TS::BP + e0, true);
+          lds_states<T, 4>(c4, ccol + r * TS::BP + e0, true);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const T av = Num<T>::exp_scaled(dj * A2v[e0 + e]);
+            const T h = fma(av, hv[e0 + e], h4[e]);
+            hv[e0 + e] = h;
+            acc = fma(c4[e], h, acc);
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < QV; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (col_ok) {
+          if (s2 == 0)
+            a.y[s * HW + static_cast<size_t>(i) * W + jg] = fma(Dsk, sg[TS::XO + r * TS::XP + j2], acc);
+          if (save && (i % K) == K - 1 && i < H - 1) {
+            T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + i / K) * W + jg) * N + s2 * SV;
+#pragma unroll
+            for (int e0 = 0; e0 < SV; e0 += 4) {
+              T v[4] = {hv[e0], hv[e0 + 1], hv[e0 + 2], hv[e0 + 3]};
+              stg_states<T, 4>(ck + e0, v, 4, true);
+            }
+          }
+          if (emit_ref && ((i % Tt) == Tt - 1 || i == H - 1)) {  // reference P^v (:217-220)
+            const size_t tile0 = (static_cast<size_t>(s) * kh + i / Tt) * kw + jg / Tt;
+#pragma unroll
+            for (int e = 0; e < SV; ++e) a.pv[(tile0 * Tt + jg % Tt) * N + s2 * SV + e] = hv[e];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (++st == nstage) st = 0;
+  }
+}
+
+}  // namespace s2d
