@@ -119,6 +119,23 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p.f = make_geo(d, false);
   p.K = std::min(env_int("SCAN2D_BAND_ROWS", 8), static_cast<int>(d.height));
   p.nb = static_cast<int>(ceil_div(d.height, p.K));
+  const int N = d.state_dim;
+  if (N == 4 || N == 8 || N == 16 || N == 32) {
+    // Fixed 16-column carry grid, whatever forward kernel runs (the
+    // tile-transpose kernel walks 16-column strips): the residual layout then
+    // depends on the descriptor only, never on pointer alignment.
+    p.Q = 16;
+    p.nq = static_cast<int>(ceil_div(d.width, 16)) - 1;
+    while (p.b.wreal > 1 && (p.b.colsw % 16) != 0 && p.b.J < 4) {
+      p.b.J *= 2;
+      p.b.colsw = p.b.cps * p.b.J;
+      p.b.wreal = static_cast<int>(ceil_div(d.width, p.b.colsw));
+      p.b.units = ceil_div(d.num_scans, p.b.seg) * p.b.wreal;
+    }
+    if (p.b.wreal > 1 && (p.b.colsw % 16) != 0) return SCAN2D_EUNSUPPORTED;
+    if ((16 % p.f.J) != 0 || (p.f.wreal > 1 && (p.f.colsw % 16) != 0)) return SCAN2D_EUNSUPPORTED;
+    return SCAN2D_OK;
+  }
   if (p.b.wreal > 1) {
     p.Q = p.b.colsw;
     p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
@@ -178,17 +195,6 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
     g.wreal = static_cast<int>(ceil_div(d.width, 16));
     g.units = d.num_scans * g.wreal;
     g.stages = env_int("SCAN2D_TILE_STAGES", 2);
-    // horizontal carries on the 16-column strip grid
-    p.Q = 16;
-    p.nq = static_cast<int>(ceil_div(d.width, 16)) - 1;
-    // the backward's column groups must sit on the same grid
-    while (p.b.wreal > 1 && (p.b.colsw % 16) != 0 && p.b.J < 4) {
-      p.b.J *= 2;
-      p.b.colsw = p.b.cps * p.b.J;
-      p.b.wreal = static_cast<int>(ceil_div(d.width, p.b.colsw));
-      p.b.units = ceil_div(d.num_scans, p.b.seg) * p.b.wreal;
-    }
-    if (p.b.wreal > 1 && (p.b.colsw % 16) != 0) return SCAN2D_EUNSUPPORTED;
     const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.stages) : s2d::tile_elems<float>(d.state_dim, g.stages);
     g.stage_elems = 0;
     g.table_off = 0;

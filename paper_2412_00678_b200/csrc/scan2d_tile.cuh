@@ -36,8 +36,9 @@ struct TileShape {
   // stage: X[R][XP] Z[R][XP] B[R][BP] C[R][BP]
   static constexpr int XO = 0, ZO = R * XP, BO = 2 * R * XP, CO = BO + R * BP;
   static constexpr int STAGE = CO + R * BP;
-  // scratch after the stages: HH[R][BP], DL[R][XP]
-  static constexpr int SCRATCH = R * BP + R * XP;
+  // hh is written in place over B (same lane reads B then writes hh), delta in
+  // place over Z: no scratch beyond the stages
+  static constexpr int SCRATCH = 0;
   static constexpr int EPV = 16 / sizeof(T);
   static constexpr int XU = R * CW / EPV;         // 16-byte units of one X (or Z) tile
   static constexpr int BU = R * CW * N / EPV;     // 16-byte units of one B (or C) tile
@@ -82,8 +83,6 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
 #pragma unroll
   for (int e = 0; e < SV; ++e) A2v[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
 
-  T* hhs = smem + nstage * TS::STAGE;  // [R][BP]
-  T* dls = hhs + R * TS::BP;           // [R][XP]
   for (int e = lane; e < nstage * TS::STAGE; e += 32) smem[e] = T(0);
   __syncwarp();
 
@@ -93,13 +92,15 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
   const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
   const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
   const int xunits_row = ncols / EPV, bunits_row = ncols * N / EPV;
+  const size_t WN = static_cast<size_t>(W) * N;
   const uint32_t sbase = smem_u32(smem);
   auto issue_tile = [&](int r0, int st) {
     const uint32_t sb = sbase + st * TS::STAGE * static_cast<int>(sizeof(T));
+    constexpr int XR = CW / EPV;  // x units per row
 #pragma unroll
     for (int m = 0; m < TS::XUL; ++m) {
       const int u = lane + 32 * m;
-      const int rr = u / (CW / EPV), cu = u % (CW / EPV);
+      const int rr = u / XR, cu = u % XR;
       if (u < TS::XU && cu < xunits_row && r0 + rr < H) {
         const size_t go = static_cast<size_t>(r0 + rr) * W + cu * EPV;
         const uint32_t so = (rr * TS::XP + cu * EPV) * sizeof(T);
@@ -107,15 +108,24 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
         cp_async16_raw(sb + (TS::ZO * sizeof(T)) + so, zg + go);
       }
     }
+    const T* bt = Bg + static_cast<size_t>(r0) * WN;
+    const T* ct = Cg + static_cast<size_t>(r0) * WN;
 #pragma unroll
     for (int m = 0; m < TS::BUL; ++m) {
-      const int u = lane + 32 * m;
-      const int rr = u / TS::BUR, cu = u % TS::BUR;
-      if (u < TS::BU && cu < bunits_row && r0 + rr < H) {
-        const size_t go = static_cast<size_t>(r0 + rr) * W * N + cu * EPV;
+      int rr, cu;
+      if constexpr (TS::BUR % 32 == 0) {
+        rr = (32 * m) / TS::BUR;
+        cu = (32 * m) % TS::BUR + lane;
+      } else {
+        const int u = lane + 32 * m;
+        rr = u / TS::BUR;
+        cu = u % TS::BUR;
+      }
+      if (cu < bunits_row && r0 + rr < H) {
+        const size_t go = rr * WN + cu * EPV;
         const uint32_t so = (rr * TS::BP + cu * EPV) * sizeof(T);
-        cp_async16_raw(sb + (TS::BO * sizeof(T)) + so, Bg + go);
-        cp_async16_raw(sb + (TS::CO * sizeof(T)) + so, Cg + go);
+        cp_async16_raw(sb + (TS::BO * sizeof(T)) + so, bt + go);
+        cp_async16_raw(sb + (TS::CO * sizeof(T)) + so, ct + go);
       }
     }
   };
@@ -135,6 +145,7 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
   for (int e = 0; e < SV; ++e) hv[e] = T(0);
 
   const int ntiles = (H + R - 1) / R;
+  int kb = 0, bi = 0;  // row within band / band index (residual checkpoints)
   for (int t = 0; t < nstage - 1; ++t) {
     if (t < ntiles) issue_tile(t * R, t);
     cp_async_commit();
@@ -160,14 +171,16 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
     }
     cp_async_wait_dyn(nstage - 1);
     __syncwarp();
-    const T* sg = smem + st * TS::STAGE;
+    T* sg = smem + st * TS::STAGE;
+    T* dls = sg + TS::ZO;  // delta, in place over z
+    T* hhs = sg + TS::BO;  // hh, in place over B
 
     // ================= phase 1: horizontal scan, lane = (row r1, states 4 q1 ..)
     // delta for the row's cells: the QH lanes of a row split its CW cells
 #pragma unroll
     for (int m = 0; m < CW / QH; ++m) {
       const int j = q1 + m * QH;
-      dls[r1 * TS::XP + j] = Num<T>::softplus(sg[TS::ZO + r1 * TS::XP + j] + bias);
+      dls[r1 * TS::XP + j] = Num<T>::softplus(dls[r1 * TS::XP + j] + bias);
     }
     __syncwarp();
     T hh[4];
@@ -185,12 +198,11 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
     {
       const T* xr = sg + TS::XO + r1 * TS::XP;
       const T* dr = dls + r1 * TS::XP;
-      const T* br = sg + TS::BO + r1 * TS::BP + q1 * 4;
-      T* hr = hhs + r1 * TS::BP + q1 * 4;
+      T* hr = hhs + r1 * TS::BP + q1 * 4;  // reads B, then overwrites it with hh
 #pragma unroll 4
       for (int j = 0; j < CW; ++j) {
         T b4[4];
-        lds_states<T, 4>(b4, br + j * N, true);
+        lds_states<T, 4>(b4, hr + j * N, true);
         const T dj = dr[j], xj = xr[j];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -225,11 +237,12 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
       const bool col_ok = j2 < ncols;
       const T* hcol = hhs + j2 * N + s2 * SV;
       const T* ccol = sg + TS::CO + j2 * N + s2 * SV;
-      for (int r = 0; r < R; ++r) {
+      T* yp = a.y + s * HW + static_cast<size_t>(r0) * W + jg;
+      const int rows = min(R, H - r0);
+      for (int r = 0; r < rows; ++r) {
         const int i = r0 + r;
-        if (i >= H) break;
         const T dj = dls[r * TS::XP + j2];
-        T acc = T(0);
+        T acc0 = T(0), acc1 = T(0);
 #pragma unroll
         for (int e0 = 0; e0 < SV; e0 += 4) {
           T h4[4], c4[4];
@@ -240,16 +253,19 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
             const T av = Num<T>::exp_scaled(dj * A2v[e0 + e]);
             const T h = fma(av, hv[e0 + e], h4[e]);
             hv[e0 + e] = h;
-            acc = fma(c4[e], h, acc);
+            if (e & 1)
+              acc1 = fma(c4[e], h, acc1);
+            else
+              acc0 = fma(c4[e], h, acc0);
           }
         }
+        T acc = acc0 + acc1;
 #pragma unroll
         for (int o = 1; o < QV; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
         if (col_ok) {
-          if (s2 == 0)
-            a.y[s * HW + static_cast<size_t>(i) * W + jg] = fma(Dsk, sg[TS::XO + r * TS::XP + j2], acc);
-          if (save && (i % K) == K - 1 && i < H - 1) {
-            T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + i / K) * W + jg) * N + s2 * SV;
+          if (s2 == 0) yp[static_cast<size_t>(r) * W] = fma(Dsk, sg[TS::XO + r * TS::XP + j2], acc);
+          if (save && kb == K - 1 && i < H - 1) {
+            T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + bi) * W + jg) * N + s2 * SV;
 #pragma unroll
             for (int e0 = 0; e0 < SV; e0 += 4) {
               T v[4] = {hv[e0], hv[e0 + 1], hv[e0 + 2], hv[e0 + 3]};
@@ -261,6 +277,10 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
 #pragma unroll
             for (int e = 0; e < SV; ++e) a.pv[(tile0 * Tt + jg % Tt) * N + s2 * SV + e] = hv[e];
           }
+        }
+        if (++kb == K) {
+          kb = 0;
+          ++bi;
         }
       }
     }
