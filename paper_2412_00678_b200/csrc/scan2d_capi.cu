@@ -113,6 +113,9 @@ int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K, bool xvec, bo
 
 // One plan serves both directions: the backward consumes the forward's
 // residual (checkpoints every K rows, carries every Q columns).
+// strip width of the tile-transpose forward = carry grid Q for N in {4,8,16,32}
+int tile_cw() { return env_int("SCAN2D_TILE_CW", 8) == 16 ? 16 : 8; }
+
 int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
   p.b = make_geo(d, true);
@@ -124,16 +127,16 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     // Fixed 16-column carry grid, whatever forward kernel runs (the
     // tile-transpose kernel walks 16-column strips): the residual layout then
     // depends on the descriptor only, never on pointer alignment.
-    p.Q = 16;
-    p.nq = static_cast<int>(ceil_div(d.width, 16)) - 1;
-    while (p.b.wreal > 1 && (p.b.colsw % 16) != 0 && p.b.J < 4) {
+    p.Q = tile_cw();
+    p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
+    while (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0 && p.b.J < 4) {
       p.b.J *= 2;
       p.b.colsw = p.b.cps * p.b.J;
       p.b.wreal = static_cast<int>(ceil_div(d.width, p.b.colsw));
       p.b.units = ceil_div(d.num_scans, p.b.seg) * p.b.wreal;
     }
-    if (p.b.wreal > 1 && (p.b.colsw % 16) != 0) return SCAN2D_EUNSUPPORTED;
-    if ((16 % p.f.J) != 0 || (p.f.wreal > 1 && (p.f.colsw % 16) != 0)) return SCAN2D_EUNSUPPORTED;
+    if (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0) return SCAN2D_EUNSUPPORTED;
+    if ((p.Q % p.f.J) != 0 || (p.f.wreal > 1 && (p.f.colsw % p.Q) != 0)) return SCAN2D_EUNSUPPORTED;
     return SCAN2D_OK;
   }
   if (p.b.wreal > 1) {
@@ -191,11 +194,12 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
     g.Np = d.state_dim;
     g.seg = 1;
     g.cps = g.cpw;
-    g.colsw = 16;
-    g.wreal = static_cast<int>(ceil_div(d.width, 16));
+    g.colsw = p.Q;
+    g.wreal = static_cast<int>(ceil_div(d.width, p.Q));
     g.units = d.num_scans * g.wreal;
     g.stages = env_int("SCAN2D_TILE_STAGES", 2);
-    const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.stages) : s2d::tile_elems<float>(d.state_dim, g.stages);
+    const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.colsw, g.stages)
+                       : s2d::tile_elems<float>(d.state_dim, g.colsw, g.stages);
     g.stage_elems = 0;
     g.table_off = 0;
     g.smem_bytes = static_cast<int>(static_cast<size_t>(el) * dtype_size(d.dtype));

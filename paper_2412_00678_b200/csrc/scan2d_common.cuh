@@ -354,6 +354,14 @@ __device__ __forceinline__ void lds_states(T (&out)[SPL], const T* p, bool vec) 
 
 template <typename T, int SPL>
 __device__ __forceinline__ void stg_states(T* p, const T (&v)[SPL], int nvalid, bool vec) {
+  if constexpr (SPL > 4 && SPL % 4 == 0 && sizeof(T) == 4) {
+    if (vec && nvalid >= SPL) {
+#pragma unroll
+      for (int e = 0; e < SPL; e += 4)
+        *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      return;
+    }
+  }
   if constexpr (SPL == 4 && sizeof(T) == 4) {
     if (vec) {
       *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);

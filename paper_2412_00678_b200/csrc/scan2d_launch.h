@@ -27,7 +27,7 @@ template <typename T>
 int band_elems(int K, int J, int SPL);
 // tile-transpose forward: shared elements for `stages` tiles, rows per tile
 template <typename T>
-int tile_elems(int N, int stages);
+int tile_elems(int N, int CW, int stages);
 template <typename T>
 int tile_rows(int N);
 

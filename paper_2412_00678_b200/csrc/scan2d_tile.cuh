@@ -243,13 +243,14 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
         const int i = r0 + r;
         const T dj = dls[r * TS::XP + j2];
         T acc0 = T(0), acc1 = T(0);
+        constexpr int V = SV < 4 ? SV : 4;  // states per shared-memory vector load
 #pragma unroll
-        for (int e0 = 0; e0 < SV; e0 += 4) {
-          T h4[4], c4[4];
-          lds_states<T, 4>(h4, hcol + r * TS::BP + e0, true);
-          lds_states<T, 4>(c4, ccol + r * TS::BP + e0, true);
+        for (int e0 = 0; e0 < SV; e0 += V) {
+          T h4[V], c4[V];
+          lds_states<T, V>(h4, hcol + r * TS::BP + e0, true);
+          lds_states<T, V>(c4, ccol + r * TS::BP + e0, true);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
+          for (int e = 0; e < V; ++e) {
             const T av = Num<T>::exp_scaled(dj * A2v[e0 + e]);
             const T h = fma(av, hv[e0 + e], h4[e]);
             hv[e0 + e] = h;
@@ -266,11 +267,7 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
           if (s2 == 0) yp[static_cast<size_t>(r) * W] = fma(Dsk, sg[TS::XO + r * TS::XP + j2], acc);
           if (save && kb == K - 1 && i < H - 1) {
             T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + bi) * W + jg) * N + s2 * SV;
-#pragma unroll
-            for (int e0 = 0; e0 < SV; e0 += 4) {
-              T v[4] = {hv[e0], hv[e0 + 1], hv[e0 + 2], hv[e0 + 3]};
-              stg_states<T, 4>(ck + e0, v, 4, true);
-            }
+            stg_states<T, SV>(ck, hv, SV, true);
           }
           if (emit_ref && ((i % Tt) == Tt - 1 || i == H - 1)) {  // reference P^v (:217-220)
             const size_t tile0 = (static_cast<size_t>(s) * kh + i / Tt) * kw + jg / Tt;
