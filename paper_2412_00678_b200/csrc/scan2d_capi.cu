@@ -114,7 +114,7 @@ int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K, bool xvec, bo
 // One plan serves both directions: the backward consumes the forward's
 // residual (checkpoints every K rows, carries every Q columns).
 // strip width of the tile-transpose forward = carry grid Q for N in {4,8,16,32}
-int tile_cw() { return env_int("SCAN2D_TILE_CW", 8) == 16 ? 16 : 8; }
+int tile_cw() { return env_int("SCAN2D_TILE_CW", 16) == 8 ? 8 : 16; }
 
 int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
@@ -129,6 +129,9 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     // depends on the descriptor only, never on pointer alignment.
     p.Q = tile_cw();
     p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
+    // checkpoints every tile (R = 128 / N rows): the tile backward's band
+    p.K = std::min(128 / N, static_cast<int>(d.height));
+    p.nb = static_cast<int>(ceil_div(d.height, p.K));
     while (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0 && p.b.J < 4) {
       p.b.J *= 2;
       p.b.colsw = p.b.cps * p.b.J;
@@ -197,13 +200,22 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
     g.colsw = p.Q;
     g.wreal = static_cast<int>(ceil_div(d.width, p.Q));
     g.units = d.num_scans * g.wreal;
-    g.stages = env_int("SCAN2D_TILE_STAGES", 2);
+    g.stages = env_int("SCAN2D_TILE_STAGES", 1);
     const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.colsw, g.stages)
                        : s2d::tile_elems<float>(d.state_dim, g.colsw, g.stages);
     g.stage_elems = 0;
     g.table_off = 0;
     g.smem_bytes = static_cast<int>(static_cast<size_t>(el) * dtype_size(d.dtype));
     if (g.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
+    if (p.Q == 16 && env_int("SCAN2D_TILE_BWD", 1) == 1) {
+      s2d::Geo& b = p.b;
+      b = g;
+      b.stages = 1;
+      const int eb = dbl ? s2d::tile_bwd_elems<double>(d.state_dim) : s2d::tile_bwd_elems<float>(d.state_dim);
+      b.smem_bytes = static_cast<int>(static_cast<size_t>(eb) * dtype_size(d.dtype));
+      if (b.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
+      return SCAN2D_OK;
+    }
     return finish_geo(p.b, d, true, p.K, xvec, bvec);
   }
   rc = finish_geo(p.f, d, false, p.K, xvec, bvec);

@@ -30,5 +30,7 @@ template <typename T>
 int tile_elems(int N, int CW, int stages);
 template <typename T>
 int tile_rows(int N);
+template <typename T>
+int tile_bwd_elems(int N);
 
 }  // namespace s2d
