@@ -114,7 +114,15 @@ int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K, bool xvec, bo
 // One plan serves both directions: the backward consumes the forward's
 // residual (checkpoints every K rows, carries every Q columns).
 // strip width of the tile-transpose forward = carry grid Q for N in {4,8,16,32}
-int tile_cw() { return env_int("SCAN2D_TILE_CW", 16) == 8 ? 8 : 16; }
+int tile_cw() { return 16; }
+
+// states per row lane of the tile kernels (SH in {2, 4}); the backward's SH sets
+// the checkpoint interval K = 32 SH / N, so it is descriptor-level
+int tile_sh(int N, bool bwd) {
+  const int dflt = bwd ? (N >= 32 ? 4 : 2) : 4;
+  const int v = env_int(bwd ? "SCAN2D_TILE_SH_B" : "SCAN2D_TILE_SH_F", dflt);
+  return (v == 2 || v == 4) && 32 * v / N >= 1 ? v : dflt;
+}
 
 int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
@@ -129,8 +137,8 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     // depends on the descriptor only, never on pointer alignment.
     p.Q = tile_cw();
     p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
-    // checkpoints every tile (R = 128 / N rows): the tile backward's band
-    p.K = std::min(128 / N, static_cast<int>(d.height));
+    // checkpoints every backward tile (R = 32 * SH / N rows)
+    p.K = std::min(32 * tile_sh(N, true) / N, static_cast<int>(d.height));
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
     while (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0 && p.b.J < 4) {
       p.b.J *= 2;
@@ -190,8 +198,8 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
     const bool dbl = d.dtype == SCAN2D_F64;
     s2d::Geo& g = p.f;
     g.tile = 1;
-    g.spl = 4;
-    g.lpc = d.state_dim / 4;
+    g.spl = tile_sh(d.state_dim, false);
+    g.lpc = d.state_dim / g.spl;
     g.cpw = 32 / g.lpc;
     g.J = 1;
     g.Np = d.state_dim;
@@ -201,19 +209,23 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
     g.wreal = static_cast<int>(ceil_div(d.width, p.Q));
     g.units = d.num_scans * g.wreal;
     g.stages = env_int("SCAN2D_TILE_STAGES", 1);
-    const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.colsw, g.stages)
-                       : s2d::tile_elems<float>(d.state_dim, g.colsw, g.stages);
+    const int el = dbl ? s2d::tile_elems<double>(d.state_dim, g.colsw, g.spl, g.stages, false)
+                       : s2d::tile_elems<float>(d.state_dim, g.colsw, g.spl, g.stages, false);
     g.stage_elems = 0;
     g.table_off = 0;
     g.smem_bytes = static_cast<int>(static_cast<size_t>(el) * dtype_size(d.dtype));
-    if (g.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
-    if (p.Q == 16 && env_int("SCAN2D_TILE_BWD", 1) == 1) {
+    if (el < 0 || g.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
+    if (env_int("SCAN2D_TILE_BWD", 1) == 1) {
       s2d::Geo& b = p.b;
       b = g;
       b.stages = 1;
-      const int eb = dbl ? s2d::tile_bwd_elems<double>(d.state_dim) : s2d::tile_bwd_elems<float>(d.state_dim);
+      b.spl = tile_sh(d.state_dim, true);
+      b.lpc = d.state_dim / b.spl;
+      b.cpw = 32 / b.lpc;
+      const int eb = dbl ? s2d::tile_elems<double>(d.state_dim, b.colsw, b.spl, 1, true)
+                         : s2d::tile_elems<float>(d.state_dim, b.colsw, b.spl, 1, true);
       b.smem_bytes = static_cast<int>(static_cast<size_t>(eb) * dtype_size(d.dtype));
-      if (b.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
+      if (eb < 0 || b.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
       return SCAN2D_OK;
     }
     return finish_geo(p.b, d, true, p.K, xvec, bvec);

@@ -352,6 +352,23 @@ __device__ __forceinline__ void lds_states(T (&out)[SPL], const T* p, bool vec) 
   for (int s = 0; s < SPL; ++s) out[s] = p[s];
 }
 
+// SPL consecutive states to shared memory (vectorised)
+template <typename T, int SPL>
+__device__ __forceinline__ void sts_states(T* p, const T (&v)[SPL]) {
+  if constexpr (sizeof(T) == 4 && SPL % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < SPL; e += 4) *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+  } else if constexpr (sizeof(T) == 4 && SPL == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else if constexpr (sizeof(T) == 8 && SPL % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < SPL; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(v[e], v[e + 1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < SPL; ++e) p[e] = v[e];
+  }
+}
+
 template <typename T, int SPL>
 __device__ __forceinline__ void stg_states(T* p, const T (&v)[SPL], int nvalid, bool vec) {
   if constexpr (SPL > 4 && SPL % 4 == 0 && sizeof(T) == 4) {

@@ -25,12 +25,8 @@ template <typename T>
 int stage_elems(int colsw, int Np, int seg, bool bwd);
 template <typename T>
 int band_elems(int K, int J, int SPL);
-// tile-transpose forward: shared elements for `stages` tiles, rows per tile
+// tile-transpose kernels: shared elements (row-lane states SH, strip width CW)
 template <typename T>
-int tile_elems(int N, int CW, int stages);
-template <typename T>
-int tile_rows(int N);
-template <typename T>
-int tile_bwd_elems(int N);
+int tile_elems(int N, int CW, int SH, int stages, bool bwd);
 
 }  // namespace s2d

@@ -24,13 +24,14 @@
 
 namespace s2d {
 
-template <typename T, int N, int CW>
+template <typename T, int N, int CW, int SH = 4>
 struct TileShape {
-  static constexpr int QH = N / 4;            // row lanes per row (4 states each)
+  static constexpr int QH = N / SH;           // row lanes per row (SH states each)
   static constexpr int R = 32 / QH;           // rows per tile
   static constexpr int QV = 32 / CW;          // column lanes per column
   static constexpr int SV = N / QV;           // states per column lane
-  static constexpr int PAD = 4 * QH;          // row padding of the [R][CW][N] blocks (floats)
+  static constexpr int PAD = N;               // row padding of the [R][CW][N] blocks (floats):
+                                              // rows of one access group land on distinct banks
   static constexpr int BP = CW * N + PAD;     // padded row pitch of B / C / HH
   static constexpr int XP = CW;               // row pitch of X / Z / DL
   // stage: X[R][XP] Z[R][XP] B[R][BP] C[R][BP]
@@ -48,9 +49,9 @@ struct TileShape {
   static_assert(QH >= 1 && R >= 1 && QV >= 1 && SV >= 1, "bad tile shape");
 };
 
-template <typename T, int N, int CW>
+template <typename T, int N, int CW, int SH>
 __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a) {
-  using TS = TileShape<T, N, CW>;
+  using TS = TileShape<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, EPV = TS::EPV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
@@ -73,13 +74,13 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
   const size_t HW = static_cast<size_t>(H) * W;
   const T Dsk = a.Dskip[p], bias = a.bias[p];
 
-  // phase-1 identity: row r1, states 4*q1 .. 4*q1+3
+  // phase-1 identity: row r1, states SH*q1 .. SH*q1+SH-1
   const int r1 = lane / QH, q1 = lane % QH;
   // phase-2 identity: column j2, states s2*SV .. s2*SV+SV-1
   const int j2 = lane / QV, s2 = lane % QV;
-  T A1[4], A2v[SV];
+  T A1[SH], A2v[SV];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * 4 + e]);
+  for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
 #pragma unroll
   for (int e = 0; e < SV; ++e) A2v[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
 
@@ -134,8 +135,8 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
   const bool save = a.ckpt != nullptr;
   const int nq = a.plan.nq, K = a.plan.K, nbm1 = a.plan.nb - 1;
   const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
-  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * 4 : nullptr;
-  CarrySlot<T>* hc_out = has_succ ? a.hcarry + ((s * nq + wpos) * H) * N + q1 * 4 : nullptr;
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * SH : nullptr;
+  CarrySlot<T>* hc_out = has_succ ? a.hcarry + ((s * nq + wpos) * H) * N + q1 * SH : nullptr;
   const bool emit_ref = a.ph != nullptr;
   const int Tt = a.T_tile;
   const int kh = (H + Tt - 1) / Tt, kw = (W + Tt - 1) / Tt;
@@ -163,11 +164,11 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
     // carry-in for this lane's row, issued before the wait so it overlaps
     const int i1 = r0 + r1;
     const bool row1_ok = i1 < H;
-    CarryPre<T, 4> cpre;
+    CarryPre<T, SH> cpre;
     if constexpr (sizeof(T) == 4) {
       if (has_pred && row1_ok)
-        carry_load<4>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
-                      *reinterpret_cast<CarryPre<float, 4>*>(&cpre));
+        carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
+                       *reinterpret_cast<CarryPre<float, SH>*>(&cpre));
     }
     cp_async_wait_dyn(nstage - 1);
     __syncwarp();
@@ -183,50 +184,43 @@ __global__ void __launch_bounds__(32, 8) scan2d_fwd_tile_kernel(const Args<T> a)
       dls[r1 * TS::XP + j] = Num<T>::softplus(dls[r1 * TS::XP + j] + bias);
     }
     __syncwarp();
-    T hh[4];
+    T hh[SH];
     if (has_pred && row1_ok) {
       if constexpr (sizeof(T) == 4) {
-        carry_resolve<4>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N), cpre,
+        carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N), cpre,
                          row_tag(a.epoch, i1), hh);
       } else {
-        carry_get_wait<T, 4>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), 4);
+        carry_get_wait<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) hh[e] = T(0);
+      for (int e = 0; e < SH; ++e) hh[e] = T(0);
     }
     {
       const T* xr = sg + TS::XO + r1 * TS::XP;
       const T* dr = dls + r1 * TS::XP;
-      T* hr = hhs + r1 * TS::BP + q1 * 4;  // reads B, then overwrites it with hh
+      T* hr = hhs + r1 * TS::BP + q1 * SH;  // reads B, then overwrites it with hh
 #pragma unroll 4
       for (int j = 0; j < CW; ++j) {
-        T b4[4];
-        lds_states<T, 4>(b4, hr + j * N, true);
+        T b4[SH];
+        lds_states<T, SH>(b4, hr + j * N, true);
         const T dj = dr[j], xj = xr[j];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < SH; ++e) {
           const T av = Num<T>::exp_scaled(dj * A1[e]);
           hh[e] = fma(av, hh[e], (dj * b4[e]) * xj);
         }
-        if (j < ncols) {
-          if constexpr (sizeof(T) == 4) {
-            *reinterpret_cast<float4*>(hr + j * N) = make_float4(hh[0], hh[1], hh[2], hh[3]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) hr[j * N + e] = hh[e];
-          }
-        }
+        if (j < ncols) sts_states<T, SH>(hr + j * N, hh);
         if (emit_ref && row1_ok && j < ncols) {  // reference P^h (engine.cpp:186-194)
           const int jg = c0 + j;
           if (jg % Tt == Tt - 1 || jg == W - 1) {
             const size_t tile0 = (static_cast<size_t>(s) * kh + i1 / Tt) * kw + jg / Tt;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) a.ph[(tile0 * Tt + i1 % Tt) * N + q1 * 4 + e] = hh[e];
+            for (int e = 0; e < SH; ++e) a.ph[(tile0 * Tt + i1 % Tt) * N + q1 * SH + e] = hh[e];
           }
         }
         if (j == ncols - 1 && has_succ && row1_ok)
-          carry_put<T, 4>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), 4);
+          carry_put<T, SH>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
       }
     }
     __syncwarp();

@@ -27,9 +27,9 @@
 
 namespace s2d {
 
-template <typename T, int N, int CW>
+template <typename T, int N, int CW, int SH = 4>
 struct TileShapeB {
-  using F = TileShape<T, N, CW>;
+  using F = TileShape<T, N, CW, SH>;
   static constexpr int QH = F::QH, R = F::R, QV = F::QV, SV = F::SV, BP = F::BP, XP = F::XP, EPV = F::EPV;
   // X | D (delta over z) | DY | SG (sigmoid) | B | G (C then G) | HH | HU[(R+1)]
   static constexpr int XO = 0, DO = R * XP, YO = 2 * R * XP, SO = 3 * R * XP;
@@ -39,9 +39,9 @@ struct TileShapeB {
   static constexpr int BUR = CW * N / EPV;
 };
 
-template <typename T, int N, int CW>
+template <typename T, int N, int CW, int SH>
 __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a) {
-  using TS = TileShapeB<T, N, CW>;
+  using TS = TileShapeB<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, EPV = TS::EPV, BP = TS::BP, XP = TS::XP;
   constexpr int V = SV < 4 ? SV : 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -66,12 +66,12 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
   const size_t HW = static_cast<size_t>(H) * W;
   const T Dsk = a.Dskip[p], bias = a.bias[p];
 
-  const int r1 = lane / QH, q1 = lane % QH;  // row lanes: row r1, states 4 q1 ..
+  const int r1 = lane / QH, q1 = lane % QH;  // row lanes: row r1, states SH q1 ..
   const int j2 = lane / QV, s2 = lane % QV;  // column lanes: column j2, states s2 SV ..
-  T A1[4], Au1[4], A2v[SV];
+  T A1[SH], Au1[SH], A2v[SV];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    Au1[e] = a.A[static_cast<int64_t>(p) * N + q1 * 4 + e];
+  for (int e = 0; e < SH; ++e) {
+    Au1[e] = a.A[static_cast<int64_t>(p) * N + q1 * SH + e];
     A1[e] = Num<T>::a_scale(Au1[e]);
   }
 #pragma unroll
@@ -128,10 +128,10 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
 
   const int nq = a.plan.nq, K = a.plan.K, nbm1 = a.plan.nb - 1;
   const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
-  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * 4 : nullptr;
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * SH : nullptr;
   const int wb = ge.wreal - 1;
-  const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * 4 : nullptr;
-  CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * 4 : nullptr;
+  const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
+  CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
   T* dBg = a.dB + s * HW * N + static_cast<size_t>(c0) * N;
   T* dCg = a.dC + s * HW * N + static_cast<size_t>(c0) * N;
   T* dxg = a.dx + s * HW + c0;
@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
   T dn[SV];  // Abar(i+1) G(i+1), carried up across tiles (column lanes)
 #pragma unroll
   for (int e = 0; e < SV; ++e) dn[e] = T(0);
-  T dA_acc[4] = {T(0), T(0), T(0), T(0)};
+  T dA_acc[SH];
+#pragma unroll
+  for (int e = 0; e < SH; ++e) dA_acc[e] = T(0);
   T dbias_acc = T(0), dD_acc = T(0);
 
   T* Xs = sm + TS::XO;
@@ -160,13 +162,15 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
     const int i1 = r0 + r1;
     const bool row_ok = r1 < rows;
     // saved forward carry (residual) and the reverse carry: loads issued early
-    T hh0[4] = {T(0), T(0), T(0), T(0)};
-    if (has_pred && row_ok) carry_get<T, 4>(hc_in + static_cast<size_t>(i1) * N, hh0, 4);
-    CarryPre<T, 4> rpre;
+    T hh0[SH];
+#pragma unroll
+    for (int e = 0; e < SH; ++e) hh0[e] = T(0);
+    if (has_pred && row_ok) carry_get<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh0, SH);
+    CarryPre<T, SH> rpre;
     if constexpr (sizeof(T) == 4) {
       if (has_succ && row_ok)
-        carry_load<4>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
-                      *reinterpret_cast<CarryPre<float, 4>*>(&rpre));
+        carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
+                       *reinterpret_cast<CarryPre<float, SH>*>(&rpre));
     }
     // checkpoint row (h at row r0 - 1) for the column lanes
     T hprev[SV];
@@ -190,24 +194,21 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
     }
     __syncwarp();
     {
-      T hh[4] = {hh0[0], hh0[1], hh0[2], hh0[3]};
+      T hh[SH];
+#pragma unroll
+      for (int e = 0; e < SH; ++e) hh[e] = hh0[e];
       const T* xr = Xs + r1 * XP;
       const T* dr = Ds + r1 * XP;
-      const T* br = Bs + r1 * BP + q1 * 4;
-      T* hr = HHs + r1 * BP + q1 * 4;
+      const T* br = Bs + r1 * BP + q1 * SH;
+      T* hr = HHs + r1 * BP + q1 * SH;
 #pragma unroll 4
       for (int j = 0; j < CW; ++j) {
-        T b4[4];
-        lds_states<T, 4>(b4, br + j * N, true);
+        T b4[SH];
+        lds_states<T, SH>(b4, br + j * N, true);
         const T dj = dr[j], xj = xr[j];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) hh[e] = fma(Num<T>::exp_scaled(dj * A1[e]), hh[e], (dj * b4[e]) * xj);
-        if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(hr + j * N) = make_float4(hh[0], hh[1], hh[2], hh[3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) hr[j * N + e] = hh[e];
-        }
+        for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(dj * A1[e]), hh[e], (dj * b4[e]) * xj);
+        sts_states<T, SH>(hr + j * N, hh);
       }
     }
     // ============ F2 (column lanes): h top -> down, rows -1 .. rows-1 into HU
@@ -278,78 +279,79 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
     __syncwarp();
     // ============ R2 (row lanes): Gh right -> left, chain rule
     {
-      T rho[4] = {T(0), T(0), T(0), T(0)};
+      T rho[SH];
+#pragma unroll
+      for (int e = 0; e < SH; ++e) rho[e] = T(0);
       if (has_succ && row_ok) {
         if constexpr (sizeof(T) == 4)
-          carry_resolve<4>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N), rpre,
-                           row_tag(a.epoch, i1), rho);
+          carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N), rpre,
+                            row_tag(a.epoch, i1), rho);
         else
-          carry_get_wait<T, 4>(rc_in + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), 4);
+          carry_get_wait<T, SH>(rc_in + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
       }
       const T* xr = Xs + r1 * XP;
       const T* dr = Ds + r1 * XP;
-      const T* br = Bs + r1 * BP + q1 * 4;
-      const T* gr = Gs + r1 * BP + q1 * 4;
-      const T* hr = HHs + r1 * BP + q1 * 4;
-      const T* ur = HUs + r1 * BP + q1 * 4;  // h(i-1): HU row r1 is tile row r1 - 1
-      T* dBrow = dBg + static_cast<size_t>(i1) * WN + q1 * 4;
-      T ddp[CW], sgb[CW];
+      const T* br = Bs + r1 * BP + q1 * SH;
+      const T* gr = Gs + r1 * BP + q1 * SH;
+      const T* hr = HHs + r1 * BP + q1 * SH;
+      const T* ur = HUs + r1 * BP + q1 * SH;  // h(i-1): HU row r1 is tile row r1 - 1
+      T* dBrow = dBg + static_cast<size_t>(i1) * WN + q1 * SH;
+      // columns in groups of QH: per-cell sums over the row's QH lanes by
+      // reduce-scatter, one finished cell per lane per group
 #pragma unroll
-      for (int j = CW - 1; j >= 0; --j) {
-        T g4[4], b4[4], hl[4], hu4[4];
-        lds_states<T, 4>(g4, gr + j * N, true);
-        lds_states<T, 4>(b4, br + j * N, true);
-        lds_states<T, 4>(hu4, ur + j * N, true);
-        if (j > 0) {
-          lds_states<T, 4>(hl, hr + (j - 1) * N, true);
-        } else {
+      for (int gs = CW - QH; gs >= 0; gs -= QH) {
+        T ddp[QH], sgb[QH];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) hl[e] = hh0[e];
+        for (int jj = QH - 1; jj >= 0; --jj) {
+          const int j = gs + jj;
+          T g4[SH], b4[SH], hl[SH], hu4[SH];
+          lds_states<T, SH>(g4, gr + j * N, true);
+          lds_states<T, SH>(b4, br + j * N, true);
+          lds_states<T, SH>(hu4, ur + j * N, true);
+          if (j > 0) {
+            lds_states<T, SH>(hl, hr + (j - 1) * N, true);
+          } else {
+#pragma unroll
+            for (int e = 0; e < SH; ++e) hl[e] = hh0[e];
+          }
+          const T dj = dr[j], xj = xr[j];
+          T dd = T(0), sg = T(0), dBv[SH];
+#pragma unroll
+          for (int e = 0; e < SH; ++e) {
+            const T av = Num<T>::exp_scaled(dj * A1[e]);
+            const T gh = g4[e] + rho[e];  // engine.cpp:346
+            rho[e] = av * gh;
+            const T dab = fma(gh, hl[e], g4[e] * hu4[e]);  // engine.cpp:383
+            if (row_ok) dA_acc[e] = fma(dab, dj * av, dA_acc[e]);
+            dd = fma(gh, b4[e] * xj, fma(dab, av * Au1[e], dd));
+            sg = fma(gh, b4[e], sg);
+            dBv[e] = gh * (dj * xj);
+          }
+          ddp[jj] = dd;
+          sgb[jj] = sg;
+          if (row_ok && j < ncols) stg_states<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv, SH, true);
         }
-        const T dj = dr[j], xj = xr[j];
-        T dd = T(0), sg = T(0), dBv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const T av = Num<T>::exp_scaled(dj * A1[e]);
-          const T gh = g4[e] + rho[e];  // engine.cpp:346
-          rho[e] = av * gh;
-          const T dab = fma(gh, hl[e], g4[e] * hu4[e]);  // engine.cpp:383
-          if (row_ok) dA_acc[e] = fma(dab, dj * av, dA_acc[e]);
-          dd = fma(gh, b4[e] * xj, fma(dab, av * Au1[e], dd));
-          sg = fma(gh, b4[e], sg);
-          dBv[e] = gh * (dj * xj);
+        const int cb = reduce_scatter<QH, QH>(ddp, q1);
+        reduce_scatter<QH, QH>(sgb, q1);
+        const int j = gs + cb;
+        if (row_ok && j < ncols) {
+          const T dv = dr[j], xv = xr[j], dyv = Ys[r1 * XP + j], sv = Ss[r1 * XP + j];
+          const T dzv = ddp[0] * sv;
+          dxg[static_cast<size_t>(i1) * W + j] = fma(Dsk, dyv, dv * sgb[0]);
+          dzg[static_cast<size_t>(i1) * W + j] = dzv;
+          dbias_acc += dzv;
+          dD_acc = fma(dyv, xv, dD_acc);
         }
-        ddp[j] = dd;
-        sgb[j] = sg;
-        if (row_ok && j < ncols) stg_states<T, 4>(dBrow + static_cast<size_t>(j) * N, dBv, 4, true);
       }
       if (has_pred && row_ok)
-        carry_put<T, 4>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), 4);
-      // per-cell sums over the row's QH lanes
-      using RS_ = RS<QH, CW>;
-      const int cb = reduce_scatter<QH, CW>(ddp, q1);
-      reduce_scatter<QH, CW>(sgb, q1);
-      if ((q1 & (RS_::kReplica - 1)) == 0 && row_ok) {
-#pragma unroll
-        for (int m = 0; m < RS_::kKeep; ++m) {
-          const int j = cb + m;
-          if (j < ncols) {
-            const T dv = dr[j], xv = xr[j], dyv = Ys[r1 * XP + j], sv = Ss[r1 * XP + j];
-            const T dzv = ddp[m] * sv;
-            dxg[static_cast<size_t>(i1) * W + j] = fma(Dsk, dyv, dv * sgb[m]);
-            dzg[static_cast<size_t>(i1) * W + j] = dzv;
-            dbias_acc += dzv;
-            dD_acc = fma(dyv, xv, dD_acc);
-          }
-        }
-      }
+        carry_put<T, SH>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
     }
     __syncwarp();
   }
 
   // ---- per-(scan, strip) partials, fixed order
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
+  for (int e = 0; e < SH; ++e)
     for (int h = QH; h < 32; h <<= 1) dA_acc[e] += __shfl_xor_sync(kFull, dA_acc[e], h);
   for (int h = 1; h < 32; h <<= 1) {
     dbias_acc += __shfl_xor_sync(kFull, dbias_acc, h);
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(32, 8) scan2d_bwd_tile_kernel(const Args<T> a)
   T* part = a.part + (static_cast<size_t>(s) * ge.wreal + wpos) * (N + 2);
   if (lane < QH) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) part[q1 * 4 + e] = dA_acc[e];
+    for (int e = 0; e < SH; ++e) part[q1 * SH + e] = dA_acc[e];
   }
   if (lane == 0) {
     part[N] = dbias_acc;
