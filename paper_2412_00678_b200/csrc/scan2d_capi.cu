@@ -116,12 +116,13 @@ int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K, bool xvec, bo
 // strip width of the tile-transpose forward = carry grid Q for N in {4,8,16,32}
 int tile_cw() { return 16; }
 
-// states per row lane of the tile kernels (SH in {2, 4}); the backward's SH sets
-// the checkpoint interval K = 32 SH / N, so it is descriptor-level
-int tile_sh(int N, bool bwd) {
-  const int dflt = bwd ? (N >= 32 ? 4 : 2) : 4;
-  const int v = env_int(bwd ? "SCAN2D_TILE_SH_B" : "SCAN2D_TILE_SH_F", dflt);
-  return (v == 2 || v == 4) && 32 * v / N >= 1 ? v : dflt;
+// states per row lane of the tile kernels (scan2d_tile2.cuh): SH = 2 for fp32
+// (16 B operand registers per column), 1 for fp64.  It fixes the tile height
+// R = 32 SH / N and so the checkpoint interval K: descriptor-level.
+int tile_sh(const scan2d_desc& d) {
+  const int dflt = d.dtype == SCAN2D_F64 ? 1 : 2;
+  const int v = env_int("SCAN2D_TILE_SH", dflt);
+  return (v == 1 || v == 2) && 32 * v / d.state_dim >= 1 ? v : dflt;
 }
 
 int make_plan(const scan2d_desc& d, Plan& p) {
@@ -138,7 +139,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     p.Q = tile_cw();
     p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
     // checkpoints every backward tile (R = 32 * SH / N rows)
-    p.K = std::min(32 * tile_sh(N, true) / N, static_cast<int>(d.height));
+    p.K = std::min(32 * tile_sh(d) / N, static_cast<int>(d.height));
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
     while (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0 && p.b.J < 4) {
       p.b.J *= 2;
@@ -185,20 +186,23 @@ void vec_flags(const scan2d_desc& d, const Plan& p, const void* x, const void* z
 
 // Tile-transpose forward (scan2d_tile.cuh): N in {4, 8, 16, 32}, 16-byte copy
 // units legal, strips of 16 columns (the carry grid Q becomes 16).
-bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec) {
+// (Reference CarryState emission -- ph / pv, only the C++ shim asks for it --
+// runs on the warp kernel instead: the residual layout is the same.)
+bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec, bool emit) {
+  if (emit) return false;
   const int N = d.state_dim;
   if (!(N == 4 || N == 8 || N == 16 || N == 32) || !xvec || !bvec) return false;
   return env_int("SCAN2D_TILE_FWD", 1) == 1;
 }
 
-int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
+int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool emit = false) {
   int rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
-  if (use_tile_fwd(d, xvec, bvec)) {
+  if (use_tile_fwd(d, xvec, bvec, emit)) {
     const bool dbl = d.dtype == SCAN2D_F64;
     s2d::Geo& g = p.f;
     g.tile = 1;
-    g.spl = tile_sh(d.state_dim, false);
+    g.spl = tile_sh(d);
     g.lpc = d.state_dim / g.spl;
     g.cpw = 32 / g.lpc;
     g.J = 1;
@@ -219,7 +223,7 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec) {
       s2d::Geo& b = p.b;
       b = g;
       b.stages = 1;
-      b.spl = tile_sh(d.state_dim, true);
+      b.spl = tile_sh(d);
       b.lpc = d.state_dim / b.spl;
       b.cpw = 32 / b.lpc;
       const int eb = dbl ? s2d::tile_elems<double>(d.state_dim, b.colsw, b.spl, 1, true)
@@ -344,7 +348,7 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   if (rc != SCAN2D_OK) return rc;
   bool xvec, bvec, yvec;
   vec_flags(d, p, x, z, nullptr, B, C, y, xvec, bvec, yvec);
-  rc = plan_with_flags(d, p, xvec, bvec);
+  rc = plan_with_flags(d, p, xvec, bvec, ph != nullptr);
   if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_FWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
@@ -451,11 +455,19 @@ extern "C" {
 
 int scan2d_check_desc(const scan2d_desc* desc) { return check_desc(desc); }
 
+// The kernel choice depends on pointer alignment (16-byte copy units), so the
+// workspace covers every plan a call with this descriptor can take.
 size_t scan2d_workspace_bytes(const scan2d_desc* desc, int op) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
-  Plan p;
-  if (plan_with_flags(*desc, p, false, false) != SCAN2D_OK) return 0;
-  return ws_layout(*desc, p, op).total;
+  size_t best = 0;
+  bool any = false;
+  for (int v = 0; v < 2; ++v) {
+    Plan p;
+    if (plan_with_flags(*desc, p, v == 1, v == 1) != SCAN2D_OK) continue;
+    any = true;
+    best = std::max(best, ws_layout(*desc, p, op).total);
+  }
+  return any ? best : 0;
 }
 
 size_t scan2d_residual_bytes(const scan2d_desc* desc) {

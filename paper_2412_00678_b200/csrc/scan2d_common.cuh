@@ -413,7 +413,9 @@ struct Geo {
   int64_t units;  // warps (= CTAs) in the launch
   int stage_elems;  // elements per pipeline stage
   int table_off;    // element offset of the copy table in shared memory
-  int smem_bytes;   // dynamic shared memory per CTA
+  int smem_bytes;   // dynamic shared memory per CTA (tile kernels: per warp)
+  int cta_warps;    // tile kernels: warps (strips) per CTA, set at launch
+  int ctas_per_scan;  // tile kernels: CTAs per scan, set at launch
 };
 
 struct Plan {

@@ -1,0 +1,854 @@
+// scan2d_tile2.cuh -- register-streamed "tile-transpose" forward and backward
+// kernels for N in {4, 8, 16, 32} (sm_100a).
+//
+// Same recurrences as the reference engine (reference.cpp:85-112,
+// engine.cpp:103-121 / :196-216 forward, engine.cpp:304-397 backward):
+//   hh(i,j) = fma(Abar, hh(i,j-1), Bbar x)      h(i,j) = fma(Abar, h(i-1,j), hh(i,j))
+//   y(i,j)  = D x + sum_d C h
+//   G  = fma(C, dy, Abar(i+1,j) G(i+1,j))      Gh = G + Abar(i,j+1) Gh(i,j+1)
+//   dAbar = Gh hh(i,j-1) + G h(i-1,j);  dA += dAbar delta Abar;  ddelta = sum_d dAbar Abar A + Gh B x
+//   dB = Gh delta x;  dC = dy h;  dx = D dy + delta sum_d Gh B;  dz = ddelta sigmoid(z+bias)
+//
+// Decomposition (one warp = one CTA = one 16-column STRIP of one scan, walking
+// the strip in tiles of R rows; R * N / SH = 32):
+//  * row lanes (r, q) own row r of the tile and SH consecutive states: they run
+//    the horizontal recurrences (hh forward, Gh backward) with the carry in
+//    registers.  Their B operands come straight from HBM into registers
+//    (8/16-byte loads, 64 contiguous bytes per row) one tile AHEAD -- B never
+//    touches shared memory;
+//  * column lanes (j, s) own column j and SV = N/2 states: they run the
+//    vertical recurrences (h forward, G backward) with the state in registers
+//    across tiles.  Their C operands stream through shared memory with
+//    cp.async, also one tile ahead;
+//  * the only transposes are hh (row -> column lanes) and G (column -> row
+//    lanes), through three rotating [R][16 N + N] slots (C of this tile, hh of
+//    this tile, C of the next tile); the padding keeps both access patterns
+//    bank-conflict free.
+//  * the backward splits dAbar = Gh hh(i,j-1) + G h(i-1,j): the column lanes
+//    fold the G h(i-1,j) half into dA and ddelta themselves (they own h), so
+//    h never has to be transposed back to the row lanes.
+//  * strips exchange the horizontal carries through global memory as tagged
+//    8-byte words (scan2d_common.cuh); tickets order the strips so every
+//    producer is resident before its consumer.  The forward publishes hh at
+//    every strip boundary (kept as the training residual) and h at the last row
+//    of every tile (checkpoints), so the backward recomputes instead of storing
+//    states.
+// Shared memory per warp (fp32, N = 16): 15.4 KB -> 13 warps per SM, so the
+// 1664 strips of a 128 x 200 x 200 batch are resident in one wave.
+#pragma once
+
+#include "scan2d_fwd.cuh"
+
+namespace s2d {
+
+template <typename T>
+struct LnScale;
+template <>
+struct LnScale<float> {
+  // A1 = A log2(e) (exp_scaled takes base-2 exponents); A = A1 ln 2
+  static constexpr float v = 0.6931471805599453f;
+};
+template <>
+struct LnScale<double> {
+  static constexpr double v = 1.0;  // fp64 keeps A unscaled (Num<double>::a_scale)
+};
+
+template <typename T, int N, int CW, int SH>
+struct T2Shape {
+  static constexpr int QH = N / SH;      // row lanes per row
+  static constexpr int R = 32 / QH;      // rows per tile
+  static constexpr int QV = 32 / CW;     // column lanes per column
+  static constexpr int SV = N / QV;      // states per column lane
+  static constexpr int BP = CW * N + N;  // padded slot row pitch (elements)
+  static constexpr int SLOT = R * BP;
+  static constexpr int CELLS = R * CW;
+  static constexpr int EPV = 16 / static_cast<int>(sizeof(T));
+  static constexpr int RG = QH < CW ? QH : CW;  // columns per reduce-scatter group (backward)
+  static constexpr int BUR = CW * N / EPV;       // 16-byte units per slot row
+  // forward:  slots[3] | X[2] | Z[2] (z, then delta in place) | DX (delta x)
+  static constexpr int F_X = 3 * SLOT, F_Z = F_X + 2 * CELLS, F_DX = F_Z + 2 * CELLS;
+  static constexpr int F_TOTAL_RAW = F_DX + CELLS;
+  static constexpr int F_TOTAL = (F_TOTAL_RAW + EPV - 1) / EPV * EPV;
+  // backward: slots[3] | X[2] | Z[2] | DY[2] | DX | SG (sigmoid) | DV (column-lane ddelta) | SCR[N]
+  static constexpr int B_X = 3 * SLOT, B_Z = B_X + 2 * CELLS, B_Y = B_Z + 2 * CELLS;
+  static constexpr int B_DX = B_Y + 2 * CELLS, B_SG = B_DX + CELLS, B_DV = B_SG + CELLS;
+  static constexpr int B_SCR = B_DV + CELLS;
+  // per-warp regions are padded to 16 bytes (cp.async destinations)
+  static constexpr int B_TOTAL = (B_SCR + N + EPV - 1) / EPV * EPV;
+  static_assert(QH >= 1 && QH <= 32 && R >= 1 && SV >= 1, "tile shape");
+  static_assert(CW % EPV == 0 && (CELLS % EPV) == 0, "16-byte copy units");
+};
+
+// ----------------------------------------------------------------- helpers
+
+// SH consecutive elements from global memory (streaming, no L1 allocation)
+template <typename T, int SH>
+__device__ __forceinline__ void ldg_states(T (&v)[SH], const T* p) {
+  if constexpr (sizeof(T) == 4 && SH % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < SH; e += 4) {
+      const float4 q = __ldcs(reinterpret_cast<const float4*>(p + e));
+      v[e] = q.x, v[e + 1] = q.y, v[e + 2] = q.z, v[e + 3] = q.w;
+    }
+  } else if constexpr (sizeof(T) == 4 && SH == 2) {
+    const float2 q = __ldcs(reinterpret_cast<const float2*>(p));
+    v[0] = q.x, v[1] = q.y;
+  } else if constexpr (sizeof(T) == 8 && SH % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < SH; e += 2) {
+      const double2 q = __ldcs(reinterpret_cast<const double2*>(p + e));
+      v[e] = q.x, v[e + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < SH; ++e) v[e] = __ldcs(p + e);
+  }
+}
+
+template <typename T, int SH>
+__device__ __forceinline__ void stg_stream(T* p, const T (&v)[SH]) {
+  if constexpr (sizeof(T) == 4 && SH % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < SH; e += 4) __stcs(reinterpret_cast<float4*>(p + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+  } else if constexpr (sizeof(T) == 4 && SH == 2) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
+  } else if constexpr (sizeof(T) == 8 && SH % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < SH; e += 2) __stcs(reinterpret_cast<double2*>(p + e), make_double2(v[e], v[e + 1]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < SH; ++e) __stcs(p + e, v[e]);
+  }
+}
+
+// V consecutive elements from / to shared memory (V a power of two)
+template <typename T, int V>
+__device__ __forceinline__ void lds_vec(T (&v)[V], const T* p) {
+  constexpr int E = 16 / static_cast<int>(sizeof(T));  // elements per 16-byte access
+  if constexpr (V % E == 0 && sizeof(T) == 4) {
+#pragma unroll
+    for (int e = 0; e < V; e += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p + e);
+      v[e] = q.x, v[e + 1] = q.y, v[e + 2] = q.z, v[e + 3] = q.w;
+    }
+  } else if constexpr (V % E == 0 && sizeof(T) == 8) {
+#pragma unroll
+    for (int e = 0; e < V; e += 2) {
+      const double2 q = *reinterpret_cast<const double2*>(p + e);
+      v[e] = q.x, v[e + 1] = q.y;
+    }
+  } else if constexpr (V == 2 && sizeof(T) == 4) {
+    const float2 q = *reinterpret_cast<const float2*>(p);
+    v[0] = q.x, v[1] = q.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) v[e] = p[e];
+  }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void sts_vec(T* p, const T (&v)[V]) {
+  constexpr int E = 16 / static_cast<int>(sizeof(T));
+  if constexpr (V % E == 0 && sizeof(T) == 4) {
+#pragma unroll
+    for (int e = 0; e < V; e += 4) *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+  } else if constexpr (V % E == 0 && sizeof(T) == 8) {
+#pragma unroll
+    for (int e = 0; e < V; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(v[e], v[e + 1]);
+  } else if constexpr (V == 2 && sizeof(T) == 4) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) p[e] = v[e];
+  }
+}
+
+// rows r0 .. r0+R-1, columns 0 .. ncols-1 of an [H][W] plane (g already offset
+// by the strip's first column) -> [R][CW] in shared memory, 16-byte units
+template <typename TS, typename T>
+__device__ __forceinline__ void issue_cells(uint32_t sdst, const T* g, int r0, int H, int W, int ncols,
+                                            int lane) {
+  constexpr int XR = TS::CELLS / TS::R / TS::EPV;  // units per row (CW / EPV)
+  constexpr int XU = TS::R * XR;
+#pragma unroll
+  for (int u0 = 0; u0 < XU; u0 += 32) {
+    const int u = u0 + lane;
+    const int rr = u / XR, cu = u % XR;
+    if ((XU % 32 == 0 || u < XU) && cu * TS::EPV < ncols && r0 + rr < H)
+      cp_async16_raw(sdst + (rr * (TS::CELLS / TS::R) + cu * TS::EPV) * static_cast<uint32_t>(sizeof(T)),
+                     g + static_cast<size_t>(r0 + rr) * W + cu * TS::EPV);
+  }
+}
+
+// rows r0 .. r0+R-1 of a [H][W][N] tensor, the strip's ncols columns (g offset
+// by c0 * N) -> one [R][BP] slot
+template <typename TS, int N, typename T>
+__device__ __forceinline__ void issue_slot(uint32_t sdst, const T* g, int r0, int H, size_t WN, int ncols,
+                                           int lane) {
+  constexpr int BUR = TS::BUR;
+  constexpr int BU = TS::R * BUR;
+  const int bunits = ncols * N / TS::EPV;
+#pragma unroll
+  for (int u0 = 0; u0 < BU; u0 += 32) {
+    int rr, cu;
+    if constexpr (BUR % 32 == 0) {
+      rr = u0 / BUR;
+      cu = u0 % BUR + lane;
+    } else {
+      const int u = u0 + lane;
+      rr = u / BUR;
+      cu = u % BUR;
+    }
+    if ((BU % 32 == 0 || u0 + lane < BU) && cu < bunits && r0 + rr < H)
+      cp_async16_raw(sdst + (rr * TS::BP + cu * TS::EPV) * static_cast<uint32_t>(sizeof(T)),
+                     g + static_cast<size_t>(r0 + rr) * WN + cu * TS::EPV);
+  }
+}
+
+// row lane's B operand for one tile: B[r0 + r1][c0 + j][q1 SH ..] for j < CW
+template <typename T, int CW, int SH>
+__device__ __forceinline__ void load_b_rows(T (&b)[CW][SH], const T* Bg, int i1, int H, size_t WN, int ncols,
+                                            int N) {
+  const bool ok = i1 < H;
+  const T* p = Bg + static_cast<size_t>(ok ? i1 : 0) * WN;
+#pragma unroll
+  for (int j = 0; j < CW; ++j) {
+    if (ok && j < ncols) {
+      ldg_states<T, SH>(b[j], p + static_cast<size_t>(j) * N);
+    } else {
+#pragma unroll
+      for (int e = 0; e < SH; ++e) b[j][e] = T(0);
+    }
+  }
+}
+
+__device__ __forceinline__ int slot_next(int s) { return s == 2 ? 0 : s + 1; }
+
+// ------------------------------------------------------------ CTA = strips
+//
+// A CTA holds `nw` warps = `nw` adjacent strips of one scan (all 13 strips of a
+// 200-wide grid).  Warps of one CTA are issued fairly by the SM, so the
+// horizontal carry chain between them stays in lockstep; the carry moves
+// through a shared-memory ring guarded by mbarriers (full: producer -> consumer,
+// empty: consumer -> producer, RING tiles deep).  Only the boundaries between
+// CTAs of one scan (grids wider than nw * 16 columns) use the tagged global
+// words, and CTAs take tickets so a producer CTA is always resident first.
+
+constexpr int kRing = 4;  // carry ring depth (tiles)
+// warps (strips) per CTA at most: 13 x 32 threads x 152 registers fit one SM's
+// register file, and 13 strips cover a 200-column grid in one CTA
+constexpr int kTileMaxWarps = 13;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Carry ring of one CTA: data [nw-1][kRing][32 lanes][SH], barriers full / empty
+// [nw-1][kRing].  Boundary b sits between warps b and b+1.
+template <typename T, int SH>
+struct CarryRing {
+  T* data;
+  uint64_t* full;
+  uint64_t* empty;
+  static __host__ __device__ size_t bytes(int nw) {
+    const size_t nb = nw > 1 ? nw - 1 : 0;
+    return nb * kRing * 32 * SH * sizeof(T) + 2 * nb * kRing * sizeof(uint64_t);
+  }
+  __device__ void setup(unsigned char* base, int nw) {
+    const int nb = nw > 1 ? nw - 1 : 0;
+    data = reinterpret_cast<T*>(base);
+    full = reinterpret_cast<uint64_t*>(base + static_cast<size_t>(nb) * kRing * 32 * SH * sizeof(T));
+    empty = full + nb * kRing;
+  }
+  // producer side: tile index u (0, 1, 2, ... in the warp's own visiting order)
+  __device__ __forceinline__ void put(int b, int u, int lane, const T (&v)[SH]) {
+    const int k = u % kRing;
+    mbar_wait(empty + b * kRing + k, ((u / kRing) & 1) ^ 1);
+    T* d = data + ((static_cast<size_t>(b) * kRing + k) * 32 + lane) * SH;
+#pragma unroll
+    for (int e = 0; e < SH; ++e) d[e] = v[e];
+    mbar_arrive(full + b * kRing + k);
+  }
+  __device__ __forceinline__ void get(int b, int u, int lane, T (&v)[SH]) {
+    const int k = u % kRing;
+    mbar_wait(full + b * kRing + k, (u / kRing) & 1);
+    const T* d = data + ((static_cast<size_t>(b) * kRing + k) * 32 + lane) * SH;
+#pragma unroll
+    for (int e = 0; e < SH; ++e) v[e] = d[e];
+    mbar_arrive(empty + b * kRing + k);
+  }
+};
+
+// CTA ticket + strip identity.  rev: strips of a scan are taken right to left
+// (backward).  Returns false for warps past the scan's last strip.
+struct StripId {
+  int64_t s;
+  int strip, wi, nw, cpos, ncta;
+};
+
+__device__ __forceinline__ StripId strip_id(const Geo& ge, int* ticket, bool rev) {
+  __shared__ int tk;
+  StripId id;
+  id.nw = blockDim.x / 32;
+  id.wi = threadIdx.x / 32;
+  id.ncta = ge.ctas_per_scan;
+  int64_t unit = blockIdx.x;
+  if (id.ncta > 1) {
+    if (threadIdx.x == 0) tk = atomicAdd(ticket, 1);
+    __syncthreads();
+    unit = tk;
+  }
+  id.s = unit / id.ncta;
+  id.cpos = static_cast<int>(unit % id.ncta);
+  if (rev) id.cpos = id.ncta - 1 - id.cpos;
+  id.strip = id.cpos * id.nw + id.wi;
+  return id;
+}
+
+// ================================================================== forward
+
+template <typename T, int N, int CW, int SH>
+__global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel(const Args<T> a) {
+  using TS = T2Shape<T, N, CW, SH>;
+  constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
+  constexpr uint32_t ES = sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& ge = a.plan.f;
+  const StripId id = strip_id(ge, a.ticket, false);
+  const int lane = threadIdx.x & 31;
+  CarryRing<T, SH> ring;
+  ring.setup(smem_raw + static_cast<size_t>(id.nw) * TS::F_TOTAL * ES, id.nw);
+  if (threadIdx.x < (id.nw - 1) * kRing) {
+    mbar_init(ring.full + threadIdx.x, 32);
+    mbar_init(ring.empty + threadIdx.x, 32);
+  }
+  __syncthreads();
+  if (id.strip >= ge.wreal) return;
+  T* sm = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(id.wi) * TS::F_TOTAL;
+  const int H = a.H, W = a.W;
+  const int64_t s = id.s;
+  const int wpos = id.strip;
+  const int c0 = wpos * CW;
+  const int ncols = min(CW, W - c0);
+  const int p = static_cast<int>(s % a.P);
+  const size_t HW = static_cast<size_t>(H) * W;
+  const size_t WN = static_cast<size_t>(W) * N;
+  const T Dsk = a.Dskip[p], bias = a.bias[p];
+
+  const int r1 = lane / QH, q1 = lane % QH;  // row lanes
+  const int j2 = lane / QV, s2 = lane % QV;  // column lanes
+  T A1[SH], A2[SV];
+#pragma unroll
+  for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
+#pragma unroll
+  for (int e = 0; e < SV; ++e) A2[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
+
+  for (int e = lane; e < TS::F_TOTAL; e += 32) sm[e] = T(0);
+  __syncwarp();
+
+  const T* xg = a.x + s * HW + c0;
+  const T* zg = a.z + s * HW + c0;
+  const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
+  const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
+  const uint32_t sbase = smem_u32(sm);
+
+  const bool save = a.ckpt != nullptr;
+  const int nq = a.plan.nq, nbm1 = a.plan.nb - 1;  // checkpoints every R rows (plan.K == R)
+  const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
+  // carry-in: ring from the warp on the left, or the global word across a CTA boundary
+  const bool pred_ring = has_pred && id.wi > 0;
+  const bool succ_ring = has_succ && id.wi + 1 < id.nw;
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * SH : nullptr;
+  CarrySlot<T>* hc_out = has_succ ? a.hcarry + ((s * nq + wpos) * H) * N + q1 * SH : nullptr;
+  const int jg2 = c0 + j2;
+  const bool col_ok = j2 < ncols;
+
+  T hv[SV];
+#pragma unroll
+  for (int e = 0; e < SV; ++e) hv[e] = T(0);
+
+  const int ntiles = (H + R - 1) / R;
+  int sc = 0;  // slot holding this tile's C; sc+1: hh of this tile; sc+2: C of the next tile
+  issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, 0, H, WN, ncols, lane);
+  issue_cells<TS>(sbase + TS::F_X * ES, xg, 0, H, W, ncols, lane);
+  issue_cells<TS>(sbase + TS::F_Z * ES, zg, 0, H, W, ncols, lane);
+  cp_async_commit();
+  T bc[CW][SH];
+  load_b_rows<T, CW, SH>(bc, Bg, r1, H, WN, ncols, N);
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int r0 = t * R;
+    const int par = t & 1;
+    const int sh = slot_next(sc), sn = slot_next(sh);
+    // ---- prefetch tile t+1: C into the free slot, x / z into the other parity
+    //      (its B operand is loaded into the same registers right after phase 1)
+    if (t + 1 < ntiles) {
+      issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, r0 + R, H, WN, ncols, lane);
+      issue_cells<TS>(sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg, r0 + R, H, W, ncols, lane);
+      issue_cells<TS>(sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, r0 + R, H, W, ncols, lane);
+    }
+    cp_async_commit();
+    const int i1 = r0 + r1;
+    const bool row_ok = i1 < H;
+    CarryPre<T, SH> cpre;
+    if constexpr (sizeof(T) == 4) {
+      if (has_pred && !pred_ring && row_ok)
+        carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
+                       *reinterpret_cast<CarryPre<float, SH>*>(&cpre));
+    }
+    cp_async_wait<1>();
+    __syncwarp();
+    T* Xs = sm + TS::F_X + par * CELLS;
+    T* Ds = sm + TS::F_Z + par * CELLS;  // z, then delta in place
+    T* DXs = sm + TS::F_DX;
+    T* Cs = sm + sc * TS::SLOT;
+    T* HHs = sm + sh * TS::SLOT;
+
+    // ---- delta = softplus(z + bias) and delta x, once per cell
+#pragma unroll
+    for (int c = lane; c < CELLS; c += 32) {
+      const T d = Num<T>::softplus(Ds[c] + bias);
+      Ds[c] = d;
+      DXs[c] = d * Xs[c];
+    }
+    __syncwarp();
+
+    // ---- phase 1 (row lanes): hh left -> right
+    T hh[SH];
+#pragma unroll
+    for (int e = 0; e < SH; ++e) hh[e] = T(0);
+    if (pred_ring) {
+      ring.get(id.wi - 1, t, lane, hh);
+      if (!row_ok) {
+#pragma unroll
+        for (int e = 0; e < SH; ++e) hh[e] = T(0);
+      }
+    } else if (has_pred && row_ok) {
+      if constexpr (sizeof(T) == 4) {
+        carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
+                          *reinterpret_cast<CarryPre<float, SH>*>(&cpre), row_tag(a.epoch, i1),
+                          *reinterpret_cast<float(*)[SH]>(hh));
+      } else {
+        carry_get_wait<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
+      }
+    }
+    {
+      const T* dr = Ds + r1 * CW;
+      const T* ur = DXs + r1 * CW;
+      T* hr = HHs + r1 * BP + q1 * SH;
+#pragma unroll
+      for (int j0 = 0; j0 < CW; j0 += 4) {
+        T d4[4], u4[4];
+        lds_vec<T, 4>(d4, dr + j0);
+        lds_vec<T, 4>(u4, ur + j0);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = j0 + jj;
+#pragma unroll
+          for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
+          if (j < ncols) sts_vec<T, SH>(hr + j * N, hh);
+        }
+      }
+      // strips other than the last are full (ncols == CW): hh is the boundary carry
+      if (succ_ring) ring.put(id.wi, t, lane, hh);
+      if (has_succ && row_ok && (save || !succ_ring))
+        carry_put<T, SH>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
+    }
+    if (t + 1 < ntiles) load_b_rows<T, CW, SH>(bc, Bg, r0 + R + r1, H, WN, ncols, N);
+    __syncwarp();
+
+    // ---- phase 2 (column lanes): h top -> down, y = D x + sum_d C h
+    {
+      const T* hcol = HHs + j2 * N + s2 * SV;
+      const T* ccol = Cs + j2 * N + s2 * SV;
+      T* yp = a.y + s * HW + static_cast<size_t>(r0) * W + jg2;
+      const int rows = min(R, H - r0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T dj = Ds[r * CW + j2];
+        T h4[SV], c4[SV];
+        lds_vec<T, SV>(h4, hcol + r * BP);
+        lds_vec<T, SV>(c4, ccol + r * BP);
+        T acc0 = T(0), acc1 = T(0);
+#pragma unroll
+        for (int e = 0; e < SV; ++e) {
+          hv[e] = fma(Num<T>::exp_scaled(dj * A2[e]), hv[e], h4[e]);
+          if (e & 1)
+            acc1 = fma(c4[e], hv[e], acc1);
+          else
+            acc0 = fma(c4[e], hv[e], acc0);
+        }
+        T acc = acc0 + acc1;
+#pragma unroll
+        for (int o = 1; o < QV; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        const int i = r0 + r;
+        if (r < rows && col_ok) {
+          if (s2 == 0) __stcs(yp + static_cast<size_t>(r) * W, fma(Dsk, Xs[r * CW + j2], acc));
+          if (save && r == R - 1 && i < H - 1) {  // checkpoint: h at the last row of every tile
+            T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + t) * W + jg2) * N + s2 * SV;
+            stg_states<T, SV>(ck, hv, SV, true);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    sc = sn;
+  }
+}
+
+// ================================================================= backward
+
+template <typename T, int N, int CW, int SH>
+__global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
+  using TS = T2Shape<T, N, CW, SH>;
+  constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
+  constexpr int RG = TS::RG;
+  constexpr uint32_t ES = sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geo& ge = a.plan.b;
+  const StripId id = strip_id(ge, a.ticket, true);
+  const int lane = threadIdx.x & 31;
+  CarryRing<T, SH> ring;
+  ring.setup(smem_raw + static_cast<size_t>(id.nw) * TS::B_TOTAL * ES, id.nw);
+  if (threadIdx.x < (id.nw - 1) * kRing) {
+    mbar_init(ring.full + threadIdx.x, 32);
+    mbar_init(ring.empty + threadIdx.x, 32);
+  }
+  __syncthreads();
+  if (id.strip >= ge.wreal) return;
+  T* sm = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(id.wi) * TS::B_TOTAL;
+  const int H = a.H, W = a.W;
+  const int64_t s = id.s;
+  const int wpos = id.strip;
+  const int c0 = wpos * CW;
+  const int ncols = min(CW, W - c0);
+  const int p = static_cast<int>(s % a.P);
+  const size_t HW = static_cast<size_t>(H) * W;
+  const size_t WN = static_cast<size_t>(W) * N;
+  const T Dsk = a.Dskip[p], bias = a.bias[p];
+  const T LN = LnScale<T>::v;
+
+  const int r1 = lane / QH, q1 = lane % QH;
+  const int j2 = lane / QV, s2 = lane % QV;
+  T A1[SH], A2[SV];
+#pragma unroll
+  for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
+#pragma unroll
+  for (int e = 0; e < SV; ++e) A2[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
+
+  for (int e = lane; e < TS::B_TOTAL; e += 32) sm[e] = T(0);
+  __syncwarp();
+
+  const T* xg = a.x + s * HW + c0;
+  const T* zg = a.z + s * HW + c0;
+  const T* yg = a.dy + s * HW + c0;
+  const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
+  const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
+  const uint32_t sbase = smem_u32(sm);
+
+  const int nq = a.plan.nq, nbm1 = a.plan.nb - 1;
+  const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
+  // reverse carry: from the warp on the right (ring) or across the CTA boundary (global)
+  const bool succ_ring = has_succ && id.wi + 1 < id.nw;
+  const bool pred_ring = has_pred && id.wi > 0;
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * SH : nullptr;
+  const int wb = ge.wreal - 1;
+  const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
+  CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
+  T* dBg = a.dB + s * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
+  T* dCg = a.dC + s * HW * N + static_cast<size_t>(c0) * N + s2 * SV;
+  T* dxg = a.dx + s * HW + c0;
+  T* dzg = a.dz + s * HW + c0;
+  const int jg2 = c0 + j2;
+  const bool col_ok = j2 < ncols;
+
+  T dn[SV];  // Abar(i+1,j) G(i+1,j), carried up across tiles (column lanes)
+  T dAc[SV];
+#pragma unroll
+  for (int e = 0; e < SV; ++e) dn[e] = T(0), dAc[e] = T(0);
+  T dAr[SH];
+#pragma unroll
+  for (int e = 0; e < SH; ++e) dAr[e] = T(0);
+  T dbias_acc = T(0), dD_acc = T(0);
+
+  const int ntiles = (H + R - 1) / R;
+  int sc = 0;  // slot with C (then G) of this tile; sc+1: hh; sc+2: C of the next tile up
+  {
+    const int rl = (ntiles - 1) * R;
+    const int par = (ntiles - 1) & 1;
+    issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, rl, H, WN, ncols, lane);
+    issue_cells<TS>(sbase + (TS::B_X + par * CELLS) * ES, xg, rl, H, W, ncols, lane);
+    issue_cells<TS>(sbase + (TS::B_Z + par * CELLS) * ES, zg, rl, H, W, ncols, lane);
+    issue_cells<TS>(sbase + (TS::B_Y + par * CELLS) * ES, yg, rl, H, W, ncols, lane);
+    cp_async_commit();
+  }
+  T bc[CW][SH];
+  load_b_rows<T, CW, SH>(bc, Bg, (ntiles - 1) * R + r1, H, WN, ncols, N);
+
+  for (int t = ntiles - 1; t >= 0; --t) {
+    const int u = ntiles - 1 - t;  // visiting index (ring phase)
+    const int r0 = t * R;
+    const int rows = min(R, H - r0);
+    const int par = t & 1;
+    const int sh = slot_next(sc), sn = slot_next(sh);
+    T bn[CW][SH];
+    if (t > 0) {
+      const int ru = r0 - R;
+      issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
+      issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane);
+      issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane);
+      issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane);
+      load_b_rows<T, CW, SH>(bn, Bg, ru + r1, H, WN, ncols, N);
+    }
+    cp_async_commit();
+    const int i1 = r0 + r1;
+    const bool row_ok = r1 < rows;
+    // saved forward carry (residual), reverse carry prefetch, checkpoint row
+    T hh0[SH];
+#pragma unroll
+    for (int e = 0; e < SH; ++e) hh0[e] = T(0);
+    if (has_pred && row_ok) carry_get<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh0, SH);
+    CarryPre<T, SH> rpre;
+    if constexpr (sizeof(T) == 4) {
+      if (has_succ && !succ_ring && row_ok)
+        carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
+                       *reinterpret_cast<CarryPre<float, SH>*>(&rpre));
+    }
+    T hp0[SV];  // h(r0 - 1, j): the forward checkpoint
+#pragma unroll
+    for (int e = 0; e < SV; ++e) hp0[e] = T(0);
+    if (t > 0 && col_ok) {
+      const T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + (t - 1)) * W + jg2) * N + s2 * SV;
+      ldg_states<T, SV>(hp0, ck);
+    }
+    cp_async_wait<1>();
+    __syncwarp();
+    T* Xs = sm + TS::B_X + par * CELLS;
+    T* Ds = sm + TS::B_Z + par * CELLS;  // z, then delta in place
+    T* Ys = sm + TS::B_Y + par * CELLS;
+    T* DXs = sm + TS::B_DX;
+    T* SGs = sm + TS::B_SG;
+    T* DVs = sm + TS::B_DV;
+    T* Cs = sm + sc * TS::SLOT;   // C, then G in place
+    T* HHs = sm + sh * TS::SLOT;  // hh
+
+    // ---- per cell: delta, sigmoid, delta x
+#pragma unroll
+    for (int c = lane; c < CELLS; c += 32) {
+      const T v = Ds[c] + bias;
+      const T d = Num<T>::softplus(v);
+      Ds[c] = d;
+      SGs[c] = Num<T>::sigmoid(v);
+      DXs[c] = d * Xs[c];
+    }
+    __syncwarp();
+
+    // ---- F1 (row lanes): hh left -> right from the saved carry
+    {
+      T hh[SH];
+#pragma unroll
+      for (int e = 0; e < SH; ++e) hh[e] = hh0[e];
+      const T* dr = Ds + r1 * CW;
+      const T* ur = DXs + r1 * CW;
+      T* hr = HHs + r1 * BP + q1 * SH;
+#pragma unroll
+      for (int j0 = 0; j0 < CW; j0 += 4) {
+        T d4[4], u4[4];
+        lds_vec<T, 4>(d4, dr + j0);
+        lds_vec<T, 4>(u4, ur + j0);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = j0 + jj;
+#pragma unroll
+          for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
+          if (j < ncols) sts_vec<T, SH>(hr + j * N, hh);
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- F2 (column lanes): h top -> down from the checkpoint; dC = dy h
+    T hc[R][SV];
+    {
+      const T* hcol = HHs + j2 * N + s2 * SV;
+      T hcur[SV];
+#pragma unroll
+      for (int e = 0; e < SV; ++e) hcur[e] = hp0[e];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T dj = Ds[r * CW + j2];
+        T h4[SV];
+        lds_vec<T, SV>(h4, hcol + r * BP);
+#pragma unroll
+        for (int e = 0; e < SV; ++e) {
+          hcur[e] = fma(Num<T>::exp_scaled(dj * A2[e]), hcur[e], h4[e]);
+          hc[r][e] = hcur[e];
+        }
+        if (col_ok && r < rows) {
+          const T dyv = Ys[r * CW + j2];
+          T dc[SV];
+#pragma unroll
+          for (int e = 0; e < SV; ++e) dc[e] = dyv * hcur[e];
+          stg_stream<T, SV>(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
+        }
+      }
+    }
+
+    // ---- R1 (column lanes): G bottom -> up (G over C in place); the G h(i-1,j)
+    //      half of dAbar goes into dA and ddelta here
+    {
+      T* gcol = Cs + j2 * N + s2 * SV;
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {
+        const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
+        T g4[SV];
+        lds_vec<T, SV>(g4, gcol + r * BP);
+        T ddv = T(0);
+#pragma unroll
+        for (int e = 0; e < SV; ++e) {
+          const T av = Num<T>::exp_scaled(dj * A2[e]);
+          const T g = fma(g4[e], dyv, dn[e]);  // engine.cpp:321
+          dn[e] = av * g;
+          const T hu = r > 0 ? hc[r > 0 ? r - 1 : 0][e] : hp0[e];
+          const T tv = g * hu * av;
+          dAc[e] = fma(tv, dj, dAc[e]);
+          ddv = fma(tv, A2[e], ddv);
+          g4[e] = g;
+        }
+#pragma unroll
+        for (int o = 1; o < QV; o <<= 1) ddv += __shfl_xor_sync(kFull, ddv, o);
+        if (col_ok) {
+          sts_vec<T, SV>(gcol + r * BP, g4);
+          if (s2 == 0) DVs[r * CW + j2] = ddv;
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- R2 (row lanes): Gh right -> left, the Gh hh(i,j-1) half, dB, per-cell sums
+    {
+      T rho[SH];
+#pragma unroll
+      for (int e = 0; e < SH; ++e) rho[e] = T(0);
+      if (succ_ring) {
+        ring.get(id.wi, u, lane, rho);
+        if (!row_ok) {
+#pragma unroll
+          for (int e = 0; e < SH; ++e) rho[e] = T(0);
+        }
+      } else if (has_succ && row_ok) {
+        if constexpr (sizeof(T) == 4)
+          carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
+                            *reinterpret_cast<CarryPre<float, SH>*>(&rpre), row_tag(a.epoch, i1),
+                            *reinterpret_cast<float(*)[SH]>(rho));
+        else
+          carry_get_wait<T, SH>(rc_in + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
+      }
+      const T* dr = Ds + r1 * CW;
+      const T* ur = DXs + r1 * CW;
+      const T* gr = Cs + r1 * BP + q1 * SH;
+      const T* hr = HHs + r1 * BP + q1 * SH;
+      T* dBrow = dBg + static_cast<size_t>(i1) * WN;
+#pragma unroll
+      for (int gs = CW - RG; gs >= 0; gs -= RG) {
+        T ddp[RG], sgb[RG];
+#pragma unroll
+        for (int jj = RG - 1; jj >= 0; --jj) {
+          const int j = gs + jj;
+          T g4[SH], hl[SH];
+          lds_vec<T, SH>(g4, gr + j * N);
+          if (j > 0) {
+            lds_vec<T, SH>(hl, hr + (j - 1) * N);
+          } else {
+#pragma unroll
+            for (int e = 0; e < SH; ++e) hl[e] = hh0[e];
+          }
+          const T dj = dr[j], uj = ur[j];
+          T dd = T(0), sg = T(0), dBv[SH];
+#pragma unroll
+          for (int e = 0; e < SH; ++e) {
+            const T av = Num<T>::exp_scaled(dj * A1[e]);
+            const T gh = g4[e] + rho[e];  // engine.cpp:346
+            rho[e] = av * gh;
+            const T th = gh * hl[e] * av;
+            dAr[e] = fma(th, dj, dAr[e]);
+            dd = fma(th, A1[e], dd);
+            sg = fma(gh, bc[j][e], sg);
+            dBv[e] = gh * uj;
+          }
+          ddp[jj] = dd;
+          sgb[jj] = sg;
+          if (row_ok && j < ncols) stg_stream<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
+        }
+        const int cb = reduce_scatter<QH, RG>(ddp, q1);
+        reduce_scatter<QH, RG>(sgb, q1);
+        constexpr int REP = RS<QH, RG>::kReplica;
+        const int j = gs + cb;
+        if (row_ok && j < ncols && (q1 & (REP - 1)) == 0) {
+          const int c = r1 * CW + j;
+          const T dv = Ds[c], xv = Xs[c], dyv = Ys[c];
+          const T dd = fma(ddp[0] + DVs[c], LN, xv * sgb[0]);  // ddelta = sum_d dAbar Abar A + x sum_d Gh B
+          const T dzv = dd * SGs[c];
+          dxg[static_cast<size_t>(i1) * W + j] = fma(Dsk, dyv, dv * sgb[0]);
+          dzg[static_cast<size_t>(i1) * W + j] = dzv;
+          dbias_acc += dzv;
+          dD_acc = fma(dyv, xv, dD_acc);
+        }
+      }
+      if (pred_ring)
+        ring.put(id.wi - 1, u, lane, rho);
+      else if (has_pred && row_ok)
+        carry_put<T, SH>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
+    }
+    __syncwarp();
+    if (t > 0) {
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+#pragma unroll
+        for (int e = 0; e < SH; ++e) bc[j][e] = bn[j][e];
+    }
+    sc = sn;
+  }
+
+  // ---- per-(scan, strip) partials, fixed order: dA = row-lane part + column-lane part
+#pragma unroll
+  for (int e = 0; e < SH; ++e)
+    for (int h = QH; h < 32; h <<= 1) dAr[e] += __shfl_xor_sync(kFull, dAr[e], h);
+#pragma unroll
+  for (int e = 0; e < SV; ++e)
+    for (int h = QV; h < 32; h <<= 1) dAc[e] += __shfl_xor_sync(kFull, dAc[e], h);
+  for (int h = 1; h < 32; h <<= 1) {
+    dbias_acc += __shfl_xor_sync(kFull, dbias_acc, h);
+    dD_acc += __shfl_xor_sync(kFull, dD_acc, h);
+  }
+  T* scr = sm + TS::B_SCR;
+  if (lane < QH) {
+#pragma unroll
+    for (int e = 0; e < SH; ++e) scr[q1 * SH + e] = dAr[e];
+  }
+  __syncwarp();
+  T* part = a.part + (static_cast<size_t>(s) * ge.wreal + wpos) * (N + 2);
+  if (lane < QV) {
+#pragma unroll
+    for (int e = 0; e < SV; ++e) part[s2 * SV + e] = scr[s2 * SV + e] + dAc[e];
+  }
+  if (lane == 0) {
+    part[N] = dbias_acc;
+    part[N + 1] = dD_acc;
+  }
+}
+
+}  // namespace s2d
