@@ -116,6 +116,15 @@ int finish_geo(s2d::Geo& g, const scan2d_desc& d, bool bwd, int K, bool xvec, bo
 // strip width of the tile-transpose forward = carry grid Q for N in {4,8,16,32}
 int tile_cw() { return 16; }
 
+// backward strip width: 16 columns (13-warp CTAs); 32-column strips (8-warp
+// CTAs, fp32, SH = 2, N <= 16) measured slower on B200 -- SCAN2D_TILE_CWB=32
+int tile_cw_bwd(const scan2d_desc& d, int sh) {
+  const bool wide = d.dtype == SCAN2D_F32 && sh == 2 && d.state_dim <= 16;
+  const int dflt = 16;
+  const int v = env_int("SCAN2D_TILE_CWB", dflt);
+  return (v == 16 || (v == 32 && wide)) ? v : dflt;
+}
+
 // states per row lane of the tile kernels (scan2d_tile2.cuh): SH = 2 for fp32
 // (16 B operand registers per column), 1 for fp64.  It fixes the tile height
 // R = 32 SH / N and so the checkpoint interval K: descriptor-level.
@@ -226,6 +235,9 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool em
       b.spl = tile_sh(d);
       b.lpc = d.state_dim / b.spl;
       b.cpw = 32 / b.lpc;
+      b.colsw = tile_cw_bwd(d, b.spl);
+      b.wreal = static_cast<int>(ceil_div(d.width, b.colsw));
+      b.units = d.num_scans * b.wreal;
       const int eb = dbl ? s2d::tile_elems<double>(d.state_dim, b.colsw, b.spl, 1, true)
                          : s2d::tile_elems<float>(d.state_dim, b.colsw, b.spl, 1, true);
       b.smem_bytes = static_cast<int>(static_cast<size_t>(eb) * dtype_size(d.dtype));

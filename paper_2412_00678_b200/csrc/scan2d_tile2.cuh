@@ -72,9 +72,9 @@ struct T2Shape {
   // backward: slots[3] | X[2] | Z[2] | DY[2] | DX | SG (sigmoid) | DV (column-lane ddelta) | SCR[N]
   static constexpr int B_X = 3 * SLOT, B_Z = B_X + 2 * CELLS, B_Y = B_Z + 2 * CELLS;
   static constexpr int B_DX = B_Y + 2 * CELLS, B_SG = B_DX + CELLS, B_DV = B_SG + CELLS;
-  static constexpr int B_SCR = B_DV + CELLS;
+  static constexpr int B_SCR = B_DV + CELLS, B_AS = B_SCR + N, B_DAC = B_AS + N;
   // per-warp regions are padded to 16 bytes (cp.async destinations)
-  static constexpr int B_TOTAL = (B_SCR + N + EPV - 1) / EPV * EPV;
+  static constexpr int B_TOTAL = (B_DAC + 32 * SV + EPV - 1) / EPV * EPV;
   static_assert(QH >= 1 && QH <= 32 && R >= 1 && SV >= 1, "tile shape");
   static_assert(CW % EPV == 0 && (CELLS % EPV) == 0, "16-byte copy units");
 };
@@ -511,8 +511,10 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 
 // ================================================================= backward
 
+// CW = 16: up to 13 warps (128 registers); CW = 32 (fp32, N <= 16): up to 8
+// warps with the register room for 32-column strips (7 strips cover 200 columns)
 template <typename T, int N, int CW, int SH>
-__global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
+__global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
   using TS = T2Shape<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
   constexpr int RG = TS::RG;
@@ -543,13 +545,16 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
 
   const int r1 = lane / QH, q1 = lane % QH;
   const int j2 = lane / QV, s2 = lane % QV;
-  T A1[SH], A2[SV];
+  T A1[SH];
 #pragma unroll
   for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
-#pragma unroll
-  for (int e = 0; e < SV; ++e) A2[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
 
   for (int e = lane; e < TS::B_TOTAL; e += 32) sm[e] = T(0);
+  __syncwarp();
+  // column lanes re-read their scaled A from shared memory in each phase (registers)
+  T* As = sm + TS::B_AS;
+  for (int e = lane; e < N; e += 32) As[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + e]);
+  T* DAs = sm + TS::B_DAC + lane * SV;  // this lane's column-lane dA accumulators
   __syncwarp();
 
   const T* xg = a.x + s * HW + c0;
@@ -564,7 +569,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
   // reverse carry: from the warp on the right (ring) or across the CTA boundary (global)
   const bool succ_ring = has_succ && id.wi + 1 < id.nw;
   const bool pred_ring = has_pred && id.wi > 0;
-  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * SH : nullptr;
+  // saved forward carries sit on the forward's 16-column grid (plan.Q)
+  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (c0 / a.plan.Q - 1)) * H) * N + q1 * SH : nullptr;
   const int wb = ge.wreal - 1;
   const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
   CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
@@ -576,9 +582,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
   const bool col_ok = j2 < ncols;
 
   T dn[SV];  // Abar(i+1,j) G(i+1,j), carried up across tiles (column lanes)
-  T dAc[SV];
 #pragma unroll
-  for (int e = 0; e < SV; ++e) dn[e] = T(0), dAc[e] = T(0);
+  for (int e = 0; e < SV; ++e) dn[e] = T(0);
   T dAr[SH];
 #pragma unroll
   for (int e = 0; e < SH; ++e) dAr[e] = T(0);
@@ -596,7 +601,6 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
     cp_async_commit();
   }
   T bc[CW][SH];
-  load_b_rows<T, CW, SH>(bc, Bg, (ntiles - 1) * R + r1, H, WN, ncols, N);
 
   for (int t = ntiles - 1; t >= 0; --t) {
     const int u = ntiles - 1 - t;  // visiting index (ring phase)
@@ -604,16 +608,17 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
     const int rows = min(R, H - r0);
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
-    T bn[CW][SH];
     if (t > 0) {
       const int ru = r0 - R;
       issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
       issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane);
       issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane);
       issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane);
-      load_b_rows<T, CW, SH>(bn, Bg, ru + r1, H, WN, ncols, N);
     }
     cp_async_commit();
+    // this tile's B operand (row lanes); registers allow no second set, so its
+    // latency overlaps the carry / checkpoint loads and the per-cell prologue
+    load_b_rows<T, CW, SH>(bc, Bg, r0 + r1, H, WN, ncols, N);
     const int i1 = r0 + r1;
     const bool row_ok = r1 < rows;
     // saved forward carry (residual), reverse carry prefetch, checkpoint row
@@ -680,61 +685,64 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
     }
     __syncwarp();
 
-    // ---- F2 (column lanes): h top -> down from the checkpoint; dC = dy h
-    T hc[R][SV];
+    // ---- CA (column lanes): G bottom -> up, over C in place (engine.cpp:321)
     {
-      const T* hcol = HHs + j2 * N + s2 * SV;
-      T hcur[SV];
+      T* gcol = Cs + j2 * N + s2 * SV;
+      T A2[SV];
+      lds_vec<T, SV>(A2, As + s2 * SV);
 #pragma unroll
-      for (int e = 0; e < SV; ++e) hcur[e] = hp0[e];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const T dj = Ds[r * CW + j2];
-        T h4[SV];
-        lds_vec<T, SV>(h4, hcol + r * BP);
+      for (int r = R - 1; r >= 0; --r) {
+        const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
+        T g4[SV];
+        lds_vec<T, SV>(g4, gcol + r * BP);
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
-          hcur[e] = fma(Num<T>::exp_scaled(dj * A2[e]), hcur[e], h4[e]);
-          hc[r][e] = hcur[e];
+          const T g = fma(g4[e], dyv, dn[e]);
+          dn[e] = Num<T>::exp_scaled(dj * A2[e]) * g;
+          g4[e] = g;
         }
+        if (col_ok) sts_vec<T, SV>(gcol + r * BP, g4);
+      }
+    }
+    // ---- CB (column lanes): h top -> down from the checkpoint, dC = dy h, and
+    //      the G h(i-1,j) half of dAbar into dA and ddelta
+    {
+      const T* hcol = HHs + j2 * N + s2 * SV;
+      const T* gcol = Cs + j2 * N + s2 * SV;
+      T hcur[SV], A2[SV], dAc[SV];
+      lds_vec<T, SV>(A2, As + s2 * SV);
+#pragma unroll
+      for (int e = 0; e < SV; ++e) hcur[e] = hp0[e], dAc[e] = T(0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
+        T h4[SV], g4[SV];
+        lds_vec<T, SV>(h4, hcol + r * BP);
+        lds_vec<T, SV>(g4, gcol + r * BP);
+        T ddv = T(0);
+#pragma unroll
+        for (int e = 0; e < SV; ++e) {
+          const T av = Num<T>::exp_scaled(dj * A2[e]);
+          const T tv = g4[e] * hcur[e] * av;  // G h(i-1,j) Abar
+          dAc[e] = fma(tv, dj, dAc[e]);
+          ddv = fma(tv, A2[e], ddv);
+          hcur[e] = fma(av, hcur[e], h4[e]);
+        }
+#pragma unroll
+        for (int o = 1; o < QV; o <<= 1) ddv += __shfl_xor_sync(kFull, ddv, o);
         if (col_ok && r < rows) {
-          const T dyv = Ys[r * CW + j2];
+          if (s2 == 0) DVs[r * CW + j2] = ddv;
           T dc[SV];
 #pragma unroll
           for (int e = 0; e < SV; ++e) dc[e] = dyv * hcur[e];
           stg_stream<T, SV>(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
         }
       }
-    }
-
-    // ---- R1 (column lanes): G bottom -> up (G over C in place); the G h(i-1,j)
-    //      half of dAbar goes into dA and ddelta here
-    {
-      T* gcol = Cs + j2 * N + s2 * SV;
+      T acc[SV];
+      lds_vec<T, SV>(acc, DAs);
 #pragma unroll
-      for (int r = R - 1; r >= 0; --r) {
-        const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
-        T g4[SV];
-        lds_vec<T, SV>(g4, gcol + r * BP);
-        T ddv = T(0);
-#pragma unroll
-        for (int e = 0; e < SV; ++e) {
-          const T av = Num<T>::exp_scaled(dj * A2[e]);
-          const T g = fma(g4[e], dyv, dn[e]);  // engine.cpp:321
-          dn[e] = av * g;
-          const T hu = r > 0 ? hc[r > 0 ? r - 1 : 0][e] : hp0[e];
-          const T tv = g * hu * av;
-          dAc[e] = fma(tv, dj, dAc[e]);
-          ddv = fma(tv, A2[e], ddv);
-          g4[e] = g;
-        }
-#pragma unroll
-        for (int o = 1; o < QV; o <<= 1) ddv += __shfl_xor_sync(kFull, ddv, o);
-        if (col_ok) {
-          sts_vec<T, SV>(gcol + r * BP, g4);
-          if (s2 == 0) DVs[r * CW + j2] = ddv;
-        }
-      }
+      for (int e = 0; e < SV; ++e) acc[e] += dAc[e];
+      sts_vec<T, SV>(DAs, acc);
     }
     __syncwarp();
 
@@ -814,12 +822,6 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
         carry_put<T, SH>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
     }
     __syncwarp();
-    if (t > 0) {
-#pragma unroll
-      for (int j = 0; j < CW; ++j)
-#pragma unroll
-        for (int e = 0; e < SH; ++e) bc[j][e] = bn[j][e];
-    }
     sc = sn;
   }
 
@@ -827,6 +829,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_bwd_tile2_kernel
 #pragma unroll
   for (int e = 0; e < SH; ++e)
     for (int h = QH; h < 32; h <<= 1) dAr[e] += __shfl_xor_sync(kFull, dAr[e], h);
+  T dAc[SV];
+  lds_vec<T, SV>(dAc, DAs);
 #pragma unroll
   for (int e = 0; e < SV; ++e)
     for (int h = QV; h < 32; h <<= 1) dAc[e] += __shfl_xor_sync(kFull, dAc[e], h);
