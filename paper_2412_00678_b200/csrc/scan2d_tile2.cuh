@@ -608,6 +608,9 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     const int rows = min(R, H - r0);
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
+    // this tile's B operand (row lanes) first: registers allow no second set, so
+    // its latency is covered by the copies, the per-cell prologue and phase CA
+    load_b_rows<T, CW, SH>(bc, Bg, r0 + r1, H, WN, ncols, N);
     if (t > 0) {
       const int ru = r0 - R;
       issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
@@ -616,9 +619,6 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
       issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane);
     }
     cp_async_commit();
-    // this tile's B operand (row lanes); registers allow no second set, so its
-    // latency overlaps the carry / checkpoint loads and the per-cell prologue
-    load_b_rows<T, CW, SH>(bc, Bg, r0 + r1, H, WN, ncols, N);
     const int i1 = r0 + r1;
     const bool row_ok = r1 < rows;
     // saved forward carry (residual), reverse carry prefetch, checkpoint row
@@ -661,6 +661,25 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     }
     __syncwarp();
 
+    // ---- CA (column lanes): G bottom -> up, over C in place (engine.cpp:321)
+    {
+      T* gcol = Cs + j2 * N + s2 * SV;
+      T A2[SV];
+      lds_vec<T, SV>(A2, As + s2 * SV);
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {
+        const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
+        T g4[SV];
+        lds_vec<T, SV>(g4, gcol + r * BP);
+#pragma unroll
+        for (int e = 0; e < SV; ++e) {
+          const T g = fma(g4[e], dyv, dn[e]);
+          dn[e] = Num<T>::exp_scaled(dj * A2[e]) * g;
+          g4[e] = g;
+        }
+        if (col_ok) sts_vec<T, SV>(gcol + r * BP, g4);
+      }
+    }
     // ---- F1 (row lanes): hh left -> right from the saved carry
     {
       T hh[SH];
@@ -685,25 +704,6 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     }
     __syncwarp();
 
-    // ---- CA (column lanes): G bottom -> up, over C in place (engine.cpp:321)
-    {
-      T* gcol = Cs + j2 * N + s2 * SV;
-      T A2[SV];
-      lds_vec<T, SV>(A2, As + s2 * SV);
-#pragma unroll
-      for (int r = R - 1; r >= 0; --r) {
-        const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
-        T g4[SV];
-        lds_vec<T, SV>(g4, gcol + r * BP);
-#pragma unroll
-        for (int e = 0; e < SV; ++e) {
-          const T g = fma(g4[e], dyv, dn[e]);
-          dn[e] = Num<T>::exp_scaled(dj * A2[e]) * g;
-          g4[e] = g;
-        }
-        if (col_ok) sts_vec<T, SV>(gcol + r * BP, g4);
-      }
-    }
     // ---- CB (column lanes): h top -> down from the checkpoint, dC = dy h, and
     //      the G h(i-1,j) half of dAbar into dA and ddelta
     {
