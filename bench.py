@@ -345,10 +345,11 @@ def main():
     fb, bb = alg_bytes(wl)
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.workload)
+    tile = op.plan()["cols_per_chunk"] == 1 and wl["N"] in (4, 8, 16, 32)
     if wl["bwd"]:
-        dom_name, dom_bytes, dom_ms = "scan2d_bwd_kernel", bb, bwd_ms
+        dom_name, dom_bytes, dom_ms = ("scan2d_bwd_tile2_kernel" if tile else "scan2d_bwd_kernel"), bb, bwd_ms
     else:
-        dom_name, dom_bytes, dom_ms = "scan2d_fwd_kernel", fb, fwd_ms
+        dom_name, dom_bytes, dom_ms = ("scan2d_fwd_tile2_kernel" if tile else "scan2d_fwd_kernel"), fb, fwd_ms
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
