@@ -109,6 +109,30 @@ int scan2d_backward(const scan2d_desc* desc, const void* x, const void* z, const
                     void* dB, void* dC, void* dDskip, void* dbias, void* workspace,
                     size_t workspace_bytes, scan2d_stream_t stream);
 
+/* ---- row-band shard: one band of rows of a taller grid ----
+ * desc->height = the band's rows.  The horizontal recurrences are band-local; the
+ * vertical ones continue across the band edges through [S][W][N] carries:
+ *   h_top     h of the row just above the band (NULL = first band, zeros)
+ *   h_bottom  forward output: h of the band's last row (= the next band's h_top)
+ *   g_bottom  backward input: Abar(i+1,j) G(i+1,j) of the row just below the band
+ *             (= the next band's g_top; NULL = last band, zeros)
+ *   g_top     backward output: Abar G of the band's first row
+ * The backward takes the same h_top as its forward.  dA / dDskip / dbias are the
+ * band's partial sums (add them over bands in a fixed order).  Tile-kernel
+ * configurations only (N in {4, 8, 16, 32}, 16-byte aligned rows); otherwise
+ * SCAN2D_EUNSUPPORTED.  A band starting at a multiple of 32 * SH / N rows of the
+ * full grid (SH = 2 fp32, 1 fp64) reproduces the full grid's y, dx, dz, dB, dC
+ * bit for bit; dA / dDskip / dbias up to the order of the band sum. */
+int scan2d_forward_band(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                        const void* C, const void* A, const void* Dskip, const void* bias,
+                        const void* h_top, void* y, void* h_bottom, void* residual, void* workspace,
+                        size_t workspace_bytes, scan2d_stream_t stream);
+int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                         const void* C, const void* A, const void* Dskip, const void* bias,
+                         const void* h_top, const void* residual, const void* dy, const void* g_bottom,
+                         void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip, void* dbias,
+                         void* g_top, void* workspace, size_t workspace_bytes, scan2d_stream_t stream);
+
 /* Typed conveniences (desc->dtype is overridden). */
 int scan2d_fwd_f32(const scan2d_desc* desc, const float* x, const float* z, const float* B,
                    const float* C, const float* A, const float* Dskip, const float* bias,

@@ -25,6 +25,8 @@ EXPORTED_SYMBOLS = (
     "scan2d_residual_bytes",
     "scan2d_forward",
     "scan2d_backward",
+    "scan2d_forward_band",
+    "scan2d_backward_band",
     "scan2d_fwd_f32",
     "scan2d_fwd_f64",
     "scan2d_bwd_f32",
@@ -78,6 +80,10 @@ def _load():
     lib.scan2d_forward.restype = C.c_int
     lib.scan2d_backward.argtypes = [D] + [P] * 17 + [C.c_size_t, P]
     lib.scan2d_backward.restype = C.c_int
+    lib.scan2d_forward_band.argtypes = [D] + [P] * 12 + [C.c_size_t, P]
+    lib.scan2d_forward_band.restype = C.c_int
+    lib.scan2d_backward_band.argtypes = [D] + [P] * 20 + [C.c_size_t, P]
+    lib.scan2d_backward_band.restype = C.c_int
     for name, n_in in (("scan2d_fwd_f32", 12), ("scan2d_fwd_f64", 12)):
         getattr(lib, name).argtypes = [D] + [P] * n_in + [C.c_size_t, P]
         getattr(lib, name).restype = C.c_int

@@ -315,3 +315,48 @@ class Scan2dFunction(torch.autograd.Function):
 
 def scan2d(x, z, B, C_, A, Dskip, bias, tile: int = 16):
     return Scan2dFunction.apply(x, z, B, C_, A, Dskip, bias, tile)
+
+
+class Scan2dBandOp:
+    """One row band of a taller grid (SURVEY.md §8e row-band shard) over the
+    C ABI's ``scan2d_forward_band`` / ``scan2d_backward_band``.
+
+    ``forward`` takes ``h_top`` [S,W,N] (h of the row above the band; None for
+    the first band) and returns ``(y, h_bottom)``; ``backward`` takes the same
+    ``h_top``, ``dy`` and ``g_bottom`` (Abar G of the row below; None for the last
+    band) and returns ``(dx, dz, dA, dB, dC, dD, dbias, g_top)``.  dA / dD / dbias
+    are this band's partial sums.  Buffers are preallocated per descriptor."""
+
+    def __init__(self, S, H, W, N, tile=16, dtype=torch.float32, device="cuda", with_backward=True):
+        self.op = Scan2dOp(S, H, W, N, tile=tile, dtype=dtype, device=device, with_backward=with_backward)
+        e = lambda *s: torch.empty(s, dtype=dtype, device=self.op.dev)
+        self.h_bottom = e(S, W, N)
+        self.g_top = e(S, W, N) if with_backward else None
+        self.launches = 0
+
+    @property
+    def desc(self):
+        return self.op.desc
+
+    def forward(self, x, z, B, C_, A, Dskip, bias, h_top=None, save=True):
+        o = self.op
+        rc = nat.lib.scan2d_forward_band(C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
+                                         _ptr(Dskip), _ptr(bias), _ptr(h_top), _ptr(o.y), _ptr(self.h_bottom),
+                                         _ptr(o.residual) if save else None, _ptr(o.wsf), o.wsf_bytes,
+                                         _stream(o.dev))
+        if rc != nat.OK:
+            raise nat.Scan2dError(rc, "scan2d_forward_band")
+        self.launches += nat.lib.scan2d_last_launch_count()
+        return o.y, self.h_bottom
+
+    def backward(self, x, z, B, C_, A, Dskip, bias, h_top, dy, g_bottom=None):
+        o = self.op
+        rc = nat.lib.scan2d_backward_band(C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
+                                          _ptr(Dskip), _ptr(bias), _ptr(h_top), _ptr(o.residual), _ptr(dy),
+                                          _ptr(g_bottom), _ptr(o.dx), _ptr(o.dz), _ptr(o.dA), _ptr(o.dB),
+                                          _ptr(o.dC), _ptr(o.dD), _ptr(o.dbias), _ptr(self.g_top), _ptr(o.wsb),
+                                          o.wsb_bytes, _stream(o.dev))
+        if rc != nat.OK:
+            raise nat.Scan2dError(rc, "scan2d_backward_band")
+        self.launches += nat.lib.scan2d_last_launch_count()
+        return o.dx, o.dz, o.dA, o.dB, o.dC, o.dD, o.dbias, self.g_top

@@ -349,7 +349,8 @@ void set_flags(Args<T>& a, bool xvec, bool bvec, bool yvec) {
 template <typename T>
 int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
                  const void* A, const void* Dskip, const void* bias, void* y, void* ph, void* pv,
-                 void* residual, void* ws, size_t ws_bytes, cudaStream_t stream) {
+                 void* residual, void* ws, size_t ws_bytes, cudaStream_t stream,
+                 const void* vtop = nullptr, void* vbot = nullptr) {
   g_last_launches = 0;
   if (!x || !z || !B || !C || !A || !Dskip || !bias || !y) return SCAN2D_EINVAL;
   if ((ph == nullptr) != (pv == nullptr)) return SCAN2D_EINVAL;
@@ -371,6 +372,9 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   a.y = static_cast<T*>(y);
   a.ph = static_cast<T*>(ph);
   a.pv = static_cast<T*>(pv);
+  if ((vtop != nullptr || vbot != nullptr) && !p.f.tile) return SCAN2D_EUNSUPPORTED;
+  a.vtop = static_cast<const T*>(vtop);
+  a.vbot = static_cast<T*>(vbot);
   a.ticket = reinterpret_cast<int*>(w + L.ticket);
   if (residual != nullptr) {
     const ResLayout R = res_layout(d, p);
@@ -399,7 +403,8 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
                   const void* C, const void* A, const void* Dskip, const void* bias,
                   const void* residual, const void* dy, void* dx, void* dz, void* dA, void* dB,
                   void* dC, void* dDskip, void* dbias, void* ws, size_t ws_bytes,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, const void* vtop = nullptr, const void* gbot = nullptr,
+                  void* gtop = nullptr) {
   g_last_launches = 0;
   if (residual == nullptr) return SCAN2D_ESTALE;
   if (!x || !z || !B || !C || !A || !Dskip || !bias || !dy) return SCAN2D_EINVAL;
@@ -424,6 +429,10 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   a.dy = static_cast<const T*>(dy);
   a.ckpt = const_cast<T*>(reinterpret_cast<const T*>(r + R.ckpt));
   a.hcarry = const_cast<s2d::CarrySlot<T>*>(reinterpret_cast<const s2d::CarrySlot<T>*>(r + R.hcarry));
+  if ((vtop != nullptr || gbot != nullptr || gtop != nullptr) && !p.b.tile) return SCAN2D_EUNSUPPORTED;
+  a.vtop = static_cast<const T*>(vtop);
+  a.gbot = static_cast<const T*>(gbot);
+  a.gtop = static_cast<T*>(gtop);
   a.dx = static_cast<T*>(dx);
   a.dz = static_cast<T*>(dz);
   T* dB_ps = static_cast<T*>(dB);
@@ -516,6 +525,35 @@ int scan2d_backward(const scan2d_desc* desc, const void* x, const void* z, const
                                  dC, dDskip, dbias, workspace, workspace_bytes, st);
   return backward_impl<float>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC,
                               dDskip, dbias, workspace, workspace_bytes, st);
+}
+
+int scan2d_forward_band(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                        const void* C, const void* A, const void* Dskip, const void* bias,
+                        const void* h_top, void* y, void* h_bottom, void* residual, void* workspace,
+                        size_t workspace_bytes, scan2d_stream_t stream) {
+  const int rc = check_desc(desc);
+  if (rc != SCAN2D_OK) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (desc->dtype == SCAN2D_F64)
+    return forward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, y, nullptr, nullptr, residual, workspace,
+                                workspace_bytes, st, h_top, h_bottom);
+  return forward_impl<float>(*desc, x, z, B, C, A, Dskip, bias, y, nullptr, nullptr, residual, workspace,
+                             workspace_bytes, st, h_top, h_bottom);
+}
+
+int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                         const void* C, const void* A, const void* Dskip, const void* bias,
+                         const void* h_top, const void* residual, const void* dy, const void* g_bottom,
+                         void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip, void* dbias,
+                         void* g_top, void* workspace, size_t workspace_bytes, scan2d_stream_t stream) {
+  const int rc = check_desc(desc);
+  if (rc != SCAN2D_OK) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (desc->dtype == SCAN2D_F64)
+    return backward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip,
+                                 dbias, workspace, workspace_bytes, st, h_top, g_bottom, g_top);
+  return backward_impl<float>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip,
+                              dbias, workspace, workspace_bytes, st, h_top, g_bottom, g_top);
 }
 
 int scan2d_fwd_f32(const scan2d_desc* desc, const float* x, const float* z, const float* B,

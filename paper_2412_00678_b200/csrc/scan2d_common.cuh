@@ -443,6 +443,11 @@ struct Args {
   T* ph;
   T* pv;
   T* ckpt;              // residual: h at the last row of each band but the last, [S][nb-1][W][N]
+  // row-band shard (one band of a taller grid): vertical carries across the band edges
+  const T* vtop;        // h of the row above the band, [S][W][N] (NULL = zeros)
+  T* vbot;              // forward: h of the band's last row, [S][W][N] (NULL = not wanted)
+  const T* gbot;        // backward: Abar G of the row below the band, [S][W][N] (NULL = zeros)
+  T* gtop;              // backward: Abar G of the band's first row, [S][W][N] (NULL = not wanted)
   CarrySlot<T>* hcarry; // horizontal carry at every Q-column boundary, [S][nq][H][N]
   // backward outputs
   T* dx;

@@ -376,9 +376,10 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   const int jg2 = c0 + j2;
   const bool col_ok = j2 < ncols;
 
-  T hv[SV];
+  T hv[SV];  // vertical state: zeros, or the row above the band (row-band shard)
 #pragma unroll
   for (int e = 0; e < SV; ++e) hv[e] = T(0);
+  if (a.vtop != nullptr && col_ok) ldg_states<T, SV>(hv, a.vtop + (s * W + jg2) * N + s2 * SV);
 
   const int ntiles = (H + R - 1) / R;
   int sc = 0;  // slot holding this tile's C; sc+1: hh of this tile; sc+2: C of the next tile
@@ -501,6 +502,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
             T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + t) * W + jg2) * N + s2 * SV;
             stg_states<T, SV>(ck, hv, SV, true);
           }
+          if (i == H - 1 && a.vbot != nullptr)  // row-band shard: the next band's vtop
+            stg_states<T, SV>(a.vbot + (s * W + jg2) * N + s2 * SV, hv, SV, true);
         }
       }
     }
@@ -584,6 +587,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
   T dn[SV];  // Abar(i+1,j) G(i+1,j), carried up across tiles (column lanes)
 #pragma unroll
   for (int e = 0; e < SV; ++e) dn[e] = T(0);
+  if (a.gbot != nullptr && col_ok) ldg_states<T, SV>(dn, a.gbot + (s * W + jg2) * N + s2 * SV);
   T dAr[SH];
 #pragma unroll
   for (int e = 0; e < SH; ++e) dAr[e] = T(0);
@@ -638,6 +642,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     if (t > 0 && col_ok) {
       const T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + (t - 1)) * W + jg2) * N + s2 * SV;
       ldg_states<T, SV>(hp0, ck);
+    } else if (a.vtop != nullptr && col_ok) {  // row-band shard: h of the row above the band
+      ldg_states<T, SV>(hp0, a.vtop + (s * W + jg2) * N + s2 * SV);
     }
     cp_async_wait<1>();
     __syncwarp();
@@ -824,6 +830,9 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     __syncwarp();
     sc = sn;
   }
+
+  if (a.gtop != nullptr && col_ok)  // row-band shard: the band above continues from here
+    stg_states<T, SV>(a.gtop + (s * W + jg2) * N + s2 * SV, dn, SV, true);
 
   // ---- per-(scan, strip) partials, fixed order: dA = row-lane part + column-lane part
 #pragma unroll

@@ -89,12 +89,26 @@ class RowBand:
         return self.r1 - self.r0
 
 
-def row_band(H: int, world: int, rank: int) -> RowBand:
-    if H < world:
+def row_band(H: int, world: int, rank: int, align: int = 1) -> RowBand:
+    """Rows of `rank`'s band: units of `align` rows dealt as evenly as possible
+    (the last band takes the remainder).  Aligning bands to the kernels' tile
+    height (32 * SH / N rows) makes the banded result bit-identical to the
+    single-GPU one (include/scan2d_cuda.h, scan2d_forward_band)."""
+    if H < world or align < 1:
         raise ValueError("row_band: fewer rows than ranks")
-    base, extra = divmod(H, world)
-    r0 = rank * base + min(rank, extra)
-    return RowBand(rank, world, r0, r0 + base + (1 if rank < extra else 0))
+    units = -(-H // align)
+    if units < world:
+        raise ValueError("row_band: fewer aligned row units than ranks")
+    base, extra = divmod(units, world)
+    u0 = rank * base + min(rank, extra)
+    u1 = u0 + base + (1 if rank < extra else 0)
+    return RowBand(rank, world, u0 * align, min(H, u1 * align))
+
+
+def band_align(N: int, dtype_bytes: int = 4) -> int:
+    """Tile height of the tile kernels: R = 32 * SH / N (SH = 2 fp32, 1 fp64)."""
+    sh = 2 if dtype_bytes == 4 else 1
+    return max(1, 32 * sh // N) if N in (4, 8, 16, 32) else 1
 
 
 def row_band_schedule(H: int, world: int):
@@ -104,4 +118,83 @@ def row_band_schedule(H: int, world: int):
     for r in range(world - 1):
         b = row_band(H, world, r)
         out.append((r, r + 1, b.r1 - 1))
+    return out
+
+
+class RowBandPipeline:
+    """Row-band shard of a batch of scans over `world` ranks (one GPU each).
+
+    Rank r owns rows [r0, r1) of every scan (row_band) and runs ``op`` -- an
+    object with ``forward(ins, h_top) -> (y, h_bottom)`` and ``backward(ins,
+    h_top, dy, g_bottom) -> (grads..., g_top)`` for one chunk of scans, e.g. a
+    ``Scan2dBandOp`` per chunk.  The only exchanges are the vertical carries:
+    forward h_bottom of rank r -> h_top of rank r+1, backward g_top of rank r+1
+    -> g_bottom of rank r, [S_chunk, W, N] per chunk, as point-to-point
+    send/recv (NCCL over NVLink on GPUs, gloo on CPU).  The S scans are split
+    into chunks so the ranks work as a pipeline: rank r computes chunk k while
+    rank r+1 computes chunk k-1; efficiency nchunks / (nchunks + world - 1).
+    Band partial sums of dA / dD / dbias are reduced over ranks in rank order
+    by the caller (``reduce_params``)."""
+
+    def __init__(self, rank: int, world: int, dist=None):
+        self.rank, self.world, self.dist = rank, world, dist
+        self.h_tops = {}
+
+    def _recv(self, like, src):
+        import torch
+
+        buf = torch.empty_like(like)
+        self.dist.recv(buf, src=src)
+        return buf
+
+    def forward(self, op, chunks, carry_shape, make_empty):
+        """chunks: list of per-chunk input tuples; carry_shape(k) -> (S_k, W, N);
+        make_empty(shape) -> tensor for received carries.  Returns per-chunk y."""
+        ys, pending = [], []
+        for k, ins in enumerate(chunks):
+            h_top = None
+            if self.rank > 0:
+                h_top = make_empty(carry_shape(k))
+                self.dist.recv(h_top, src=self.rank - 1)
+            self.h_tops[k] = h_top
+            y, h_bot = op(k).forward(*ins, h_top=h_top)
+            ys.append(y.clone())
+            if self.rank < self.world - 1:
+                pending.append(self.dist.isend(h_bot.clone(), dst=self.rank + 1))
+        for p in pending:
+            p.wait()
+        return ys
+
+    def backward(self, op, chunks, dys, carry_shape, make_empty):
+        """Reverse carries; returns per-chunk gradient tuples (band partial sums
+        for the parameter gradients)."""
+        outs, pending = [], []
+        for k, ins in enumerate(chunks):
+            g_bot = None
+            if self.rank < self.world - 1:
+                g_bot = make_empty(carry_shape(k))
+                self.dist.recv(g_bot, src=self.rank + 1)
+            res = op(k).backward(*ins, h_top=self.h_tops.get(k), dy=dys[k], g_bottom=g_bot)
+            *grads, g_top = res
+            outs.append(tuple(g.clone() for g in grads))
+            if self.rank > 0:
+                pending.append(self.dist.isend(g_top.clone(), dst=self.rank - 1))
+        for p in pending:
+            p.wait()
+        return outs
+
+
+def reduce_params(dist, parts, world: int):
+    """Deterministic sum of per-rank parameter-gradient partials (dA, dD, dbias):
+    gather to every rank, add in rank order."""
+    import torch
+
+    out = []
+    for t in parts:
+        bufs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(bufs, t.contiguous())
+        acc = bufs[0].clone()
+        for b in bufs[1:]:
+            acc += b
+        out.append(acc)
     return out
