@@ -250,6 +250,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--rowband", action="store_true",
+                    help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), "
+                         "vertical carries exchanged point to point, pipelined over scan chunks")
+    ap.add_argument("--chunks", type=int, default=8, help="scan chunks of the row-band pipeline")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     rank = int(os.environ.get("RANK", "0"))
@@ -258,6 +262,9 @@ def main():
     config = {"workload": args.workload, "desc": wl["desc"], "S_per_gpu": wl["S"], "H": wl["H"], "W": wl["W"],
               "N": wl["N"], "tile": 16, "pass": "fwd+bwd" if wl["bwd"] else "fwd",
               "parallelism": f"scan-sharded x{world} (no collectives)"}
+
+    if args.rowband and args.impl == "ours":
+        return rowband_main(args, wl, rank, world, local, config)
 
     if args.impl == "reference":
         if rank != 0:
@@ -420,6 +427,85 @@ def main():
                 "data": "synthetic (random_instance distribution, generated on device)",
                 "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, **extra}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def rowband_main(args, wl, rank, world, local, config):
+    """Row-band shard: rank r owns rows row_band(H, world, r) of every
+    scan; carries move r -> r+1 (forward) and r+1 -> r (backward) as NCCL
+    send/recv over NVLink, pipelined over scan chunks."""
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2412_00678_b200.api import Scan2dBandOp
+    from paper_2412_00678_b200.launcher import RowBandPipeline, band_align, row_band
+
+    S, H, W, N = wl["S"], wl["H"], wl["W"], wl["N"]
+    band = row_band(H, world, rank, band_align(N))
+    nch = max(1, min(args.chunks, S))
+    cs = -(-S // nch)
+    sizes = [min(cs, S - k * cs) for k in range(nch) if k * cs < S]
+    chunks, dys, ops = [], [], []
+    for k, sk in enumerate(sizes):
+        bw = dict(wl, S=sk, H=band.rows)
+        ins, dy = synth_inputs(torch, bw, dev, 1234 + 97 * k + rank, torch.float32)
+        chunks.append(tuple(ins))
+        dys.append(dy)
+        ops.append(Scan2dBandOp(sk, band.rows, W, N, device=dev, with_backward=wl["bwd"]))
+    pipe = RowBandPipeline(rank, world, dist, streams=[torch.cuda.Stream(dev) for _ in range(len(sizes))])
+    shape = lambda k: (sizes[k], W, N)
+    mk = lambda sh: torch.empty(sh, dtype=torch.float32, device=dev)
+
+    class _Fwd:  # forward-only workloads do not keep outputs per chunk
+        def __init__(self, op):
+            self.op = op
+
+        def forward(self, *ins, h_top=None):
+            return self.op.forward(*ins, h_top=h_top, save=wl["bwd"])
+
+        def backward(self, *a, **k):
+            return self.op.backward(*a, **k)
+
+    def step():
+        pipe.forward(lambda k: _Fwd(ops[k]), chunks, shape, mk, keep=False)
+        if wl["bwd"]:
+            pipe.backward(lambda k: ops[k], chunks, dys, shape, mk, keep=False)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    if rank == 0:
+        fb, bb = alg_bytes(wl)
+        config.update({"parallelism": f"row-band x{world} (p2p vertical carries, {len(sizes)} scan chunks)",
+                       "band_rows": band.rows})
+        line = {"metric": METRIC, "value": S * H * W / (ms * 1e-3) / 1e9, "unit": "Gelem/s", "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (random_instance distribution, generated on device)", "config": config,
+                "hbm_gbs_per_gpu": (fb + (bb if wl["bwd"] else 0)) / world / (ms * 1e-3) / 1e9}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

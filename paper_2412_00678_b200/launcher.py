@@ -136,52 +136,71 @@ class RowBandPipeline:
     Band partial sums of dA / dD / dbias are reduced over ranks in rank order
     by the caller (``reduce_params``)."""
 
-    def __init__(self, rank: int, world: int, dist=None):
+    def __init__(self, rank: int, world: int, dist=None, streams=None):
         self.rank, self.world, self.dist = rank, world, dist
+        self.streams = streams  # optional pool of torch.cuda.Stream (one chunk per stream)
         self.h_tops = {}
 
-    def _recv(self, like, src):
+    def _ctx(self, k):
+        import contextlib
+
         import torch
 
-        buf = torch.empty_like(like)
-        self.dist.recv(buf, src=src)
-        return buf
+        if self.streams is None:
+            return contextlib.nullcontext()
+        return torch.cuda.stream(self.streams[k % len(self.streams)])
 
-    def forward(self, op, chunks, carry_shape, make_empty):
+    def forward(self, op, chunks, carry_shape, make_empty, keep=True):
         """chunks: list of per-chunk input tuples; carry_shape(k) -> (S_k, W, N);
-        make_empty(shape) -> tensor for received carries.  Returns per-chunk y."""
+        make_empty(shape) -> tensor for received carries.  Returns per-chunk y.
+        On GPUs every chunk runs on its own stream of the pool, so chunks overlap
+        on the device and the receive of chunk k+1 overlaps chunk k's kernels."""
         ys, pending = [], []
         for k, ins in enumerate(chunks):
-            h_top = None
-            if self.rank > 0:
-                h_top = make_empty(carry_shape(k))
-                self.dist.recv(h_top, src=self.rank - 1)
-            self.h_tops[k] = h_top
-            y, h_bot = op(k).forward(*ins, h_top=h_top)
-            ys.append(y.clone())
-            if self.rank < self.world - 1:
-                pending.append(self.dist.isend(h_bot.clone(), dst=self.rank + 1))
+            with self._ctx(k):
+                h_top = None
+                if self.rank > 0:
+                    h_top = make_empty(carry_shape(k))
+                    self.dist.irecv(h_top, src=self.rank - 1).wait()
+                self.h_tops[k] = h_top
+                y, h_bot = op(k).forward(*ins, h_top=h_top)
+                if keep:
+                    ys.append(y.clone())
+                if self.rank < self.world - 1:
+                    pending.append(self.dist.isend(h_bot, dst=self.rank + 1))
         for p in pending:
             p.wait()
+        self._join()
         return ys
 
-    def backward(self, op, chunks, dys, carry_shape, make_empty):
+    def backward(self, op, chunks, dys, carry_shape, make_empty, keep=True):
         """Reverse carries; returns per-chunk gradient tuples (band partial sums
         for the parameter gradients)."""
         outs, pending = [], []
         for k, ins in enumerate(chunks):
-            g_bot = None
-            if self.rank < self.world - 1:
-                g_bot = make_empty(carry_shape(k))
-                self.dist.recv(g_bot, src=self.rank + 1)
-            res = op(k).backward(*ins, h_top=self.h_tops.get(k), dy=dys[k], g_bottom=g_bot)
-            *grads, g_top = res
-            outs.append(tuple(g.clone() for g in grads))
-            if self.rank > 0:
-                pending.append(self.dist.isend(g_top.clone(), dst=self.rank - 1))
+            with self._ctx(k):
+                g_bot = None
+                if self.rank < self.world - 1:
+                    g_bot = make_empty(carry_shape(k))
+                    self.dist.irecv(g_bot, src=self.rank + 1).wait()
+                res = op(k).backward(*ins, h_top=self.h_tops.get(k), dy=dys[k], g_bottom=g_bot)
+                *grads, g_top = res
+                if keep:
+                    outs.append(tuple(g.clone() for g in grads))
+                if self.rank > 0:
+                    pending.append(self.dist.isend(g_top, dst=self.rank - 1))
         for p in pending:
             p.wait()
+        self._join()
         return outs
+
+    def _join(self):
+        if self.streams is not None:
+            import torch
+
+            cur = torch.cuda.current_stream()
+            for st in self.streams:
+                cur.wait_stream(st)
 
 
 def reduce_params(dist, parts, world: int):
