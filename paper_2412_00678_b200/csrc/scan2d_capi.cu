@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <initializer_list>
 #include <atomic>
 #include <cstdlib>
 #include <cstdint>
@@ -134,10 +135,26 @@ int tile_sh(const scan2d_desc& d) {
   return (v == 1 || v == 2) && 32 * v / d.state_dim >= 1 ? v : dflt;
 }
 
+// N = 1 grids up to 128 columns run the row-sweep kernels (scan2d_rows1.cuh):
+// a warp owns whole scans, so there are no horizontal carries; h is
+// checkpointed every 4 rows.  The warp kernels (reference CarryState emission)
+// accept the same residual layout.
+bool rows1_shape(const scan2d_desc& d) {
+  return d.state_dim == 1 && d.width <= 128 && env_int("SCAN2D_ROWS1", 1) == 1;
+}
+
 int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
   p.b = make_geo(d, true);
   p.f = make_geo(d, false);
+  if (rows1_shape(d)) {
+    p.K = 4;
+    p.nb = static_cast<int>(ceil_div(d.height, p.K));
+    p.Q = d.width;
+    p.nq = 0;
+    if (p.f.wreal > 1 || p.b.wreal > 1) return SCAN2D_EUNSUPPORTED;  // cannot happen for W <= 128
+    return SCAN2D_OK;
+  }
   p.K = std::min(env_int("SCAN2D_BAND_ROWS", 8), static_cast<int>(d.height));
   p.nb = static_cast<int>(ceil_div(d.height, p.K));
   const int N = d.state_dim;
@@ -204,9 +221,54 @@ bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec, bool emit) {
   return env_int("SCAN2D_TILE_FWD", 1) == 1;
 }
 
-int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool emit = false) {
+// J columns per lane: 16-byte loads when rows and pointers allow, else 8 / 4.
+// Returns false when no J puts a row on <= 32 lanes (wide odd grids: warp kernels).
+bool rows1_geo(s2d::Geo& g, const scan2d_desc& d, int align_bytes) {
+  const int es = static_cast<int>(dtype_size(d.dtype));
+  int J = 0;
+  for (int j : {4, 2, 1}) {
+    if (d.width % j == 0 && j * es <= 16 && align_bytes % (j * es) == 0 && d.width / j <= 32) {
+      J = j;
+      break;
+    }
+  }
+  if (J == 0) return false;
+  g = s2d::Geo{};
+  g.rows1 = 1;
+  g.J = J;
+  g.cps = std::max(8, next_pow2(d.width / J));  // lanes per scan (shuffle segment)
+  g.seg = 32 / g.cps;                            // scans per warp
+  g.wreal = 1;
+  g.colsw = d.width;
+  g.units = ceil_div(d.num_scans, g.seg);
+  g.smem_bytes = 0;
+  return true;
+}
+
+// largest power of two <= 16 dividing every address (x-like and B-like operands)
+int ptr_align(std::initializer_list<const void*> ps) {
+  int a = 16;
+  for (const void* q : ps) {
+    if (q == nullptr) continue;
+    const uintptr_t v = reinterpret_cast<uintptr_t>(q);
+    while (a > 1 && (v % a) != 0) a >>= 1;
+  }
+  return a;
+}
+
+int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool emit = false,
+                    int align_bytes = 16) {
   int rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
+  if (rows1_shape(d)) {
+    s2d::Geo gb;
+    if (rows1_geo(gb, d, align_bytes)) {
+      p.b = gb;
+      if (emit) return finish_geo(p.f, d, false, p.K, xvec, bvec);
+      p.f = gb;
+      return SCAN2D_OK;
+    }
+  }
   if (use_tile_fwd(d, xvec, bvec, emit)) {
     const bool dbl = d.dtype == SCAN2D_F64;
     s2d::Geo& g = p.f;
@@ -361,7 +423,7 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   if (rc != SCAN2D_OK) return rc;
   bool xvec, bvec, yvec;
   vec_flags(d, p, x, z, nullptr, B, C, y, xvec, bvec, yvec);
-  rc = plan_with_flags(d, p, xvec, bvec, ph != nullptr);
+  rc = plan_with_flags(d, p, xvec, bvec, ph != nullptr, ptr_align({x, z, B, C, y}));
   if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_FWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
@@ -416,7 +478,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   if (rc != SCAN2D_OK) return rc;
   bool xvec, bvec, yvec;
   vec_flags(d, p, x, z, dy, B, C, nullptr, xvec, bvec, yvec);
-  rc = plan_with_flags(d, p, xvec, bvec);
+  rc = plan_with_flags(d, p, xvec, bvec, false, ptr_align({x, z, B, C, dy, dx, dz, dB, dC}));
   if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;

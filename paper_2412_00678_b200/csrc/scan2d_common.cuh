@@ -402,7 +402,8 @@ __device__ __forceinline__ void stg_states(T* p, const T (&v)[SPL], int nvalid, 
 // (or `seg` whole narrow scans); lanes = (chunk, state group): SPL states of
 // J consecutive columns per lane, LPC lanes per chunk, CPW = 32/LPC chunks.
 struct Geo {
-  int tile;     // 1: tile-transpose forward kernel (scan2d_tile.cuh), CW = colsw
+  int tile;     // 1: tile kernels (scan2d_tile2.cuh), CW = colsw
+  int rows1;    // 1: N = 1 row-sweep kernels (scan2d_rows1.cuh): J columns per lane, `seg` lanes per scan
   int spl, lpc, cpw, J;
   int Np;       // states padded to spl * lpc (zero-filled in shared memory)
   int seg;      // scans packed per warp (power of two)
