@@ -223,10 +223,14 @@ bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec, bool emit) {
 
 // J columns per lane: 16-byte loads when rows and pointers allow, else 8 / 4.
 // Returns false when no J puts a row on <= 32 lanes (wide odd grids: warp kernels).
-bool rows1_geo(s2d::Geo& g, const scan2d_desc& d, int align_bytes) {
+// The forward prefers J = 2 (more warps; measured faster at 56 and 28 columns),
+// the backward J = 4 (more work per lane between its shuffle scans).
+bool rows1_geo(s2d::Geo& g, const scan2d_desc& d, int align_bytes, bool bwd) {
   const int es = static_cast<int>(dtype_size(d.dtype));
+  const int jmax = env_int(bwd ? "SCAN2D_ROWS1_JB" : "SCAN2D_ROWS1_JF", bwd ? 4 : 2);
   int J = 0;
   for (int j : {4, 2, 1}) {
+    if (j > jmax) continue;
     if (d.width % j == 0 && j * es <= 16 && align_bytes % (j * es) == 0 && d.width / j <= 32) {
       J = j;
       break;
@@ -261,11 +265,11 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool em
   int rc = make_plan(d, p);
   if (rc != SCAN2D_OK) return rc;
   if (rows1_shape(d)) {
-    s2d::Geo gb;
-    if (rows1_geo(gb, d, align_bytes)) {
+    s2d::Geo gb, gf;
+    if (rows1_geo(gb, d, align_bytes, true) && rows1_geo(gf, d, align_bytes, false)) {
       p.b = gb;
       if (emit) return finish_geo(p.f, d, false, p.K, xvec, bvec);
-      p.f = gb;
+      p.f = gf;
       return SCAN2D_OK;
     }
   }

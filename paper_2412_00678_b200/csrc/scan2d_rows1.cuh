@@ -153,7 +153,14 @@ __global__ void __launch_bounds__(128) scan2d_fwd_rows1_kernel(const Args<T> a) 
           if (ck != nullptr && r == K - 1 && i < H - 1) stg_row<T, J>(ck + static_cast<size_t>(i / K) * W, h);
           if (a.vbot != nullptr && i == H - 1) stg_row<T, J>(a.vbot + s * W + q * J, h);
         }
-        // refill this slot with row i + K
+        // L2 prefetch of row i + 2K, then refill this slot with row i + K
+        if (ok && i + 2 * K < H) {
+          const size_t o2 = static_cast<size_t>(i + 2 * K) * W;
+          prefetch_l2(xg + o2);
+          prefetch_l2(zg + o2);
+          prefetch_l2(Bg + o2);
+          prefetch_l2(Cg + o2);
+        }
         const int in = i + K;
         const bool rv = ok && in < H;
         const size_t o = static_cast<size_t>(rv ? in : 0) * W;
@@ -188,7 +195,7 @@ __device__ __forceinline__ void load_job(Rows1Job<T, J>& jb, const T* xg, const 
 }
 
 template <typename T, int J, int SEG>
-__global__ void __launch_bounds__(128) scan2d_bwd_rows1_kernel(const Args<T> a) {
+__global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> a) {
   constexpr int K = kRows1K;
   const int H = a.H, W = a.W, WJ = W / J;
   const Rows1Id id = rows1_id<SEG>(a.S, WJ);
@@ -218,10 +225,21 @@ __global__ void __launch_bounds__(128) scan2d_bwd_rows1_kernel(const Args<T> a) 
   if (a.gbot != nullptr && ok) ldg_states<T, J>(dn, a.gbot + s * W + q * J);
   T dA_acc = T(0), db_acc = T(0), dD_acc = T(0);
 
-  // job order per band: F rows r0 .. r0+K-1, then R rows r0+K-1 .. r0; loads run
-  // one job ahead in ping-pong registers (8 jobs per band: the parity is static)
-  Rows1Job<T, J> jA, jB;
-  load_job<T, J>(jA, xg, zg, Bg, Cg, yg, (nb - 1) * K, H, W, ok, false);
+  // job order per band: F rows r0 .. r0+K-1, then R rows r0+K-1 .. r0.  Loads run
+  // NB - 1 jobs ahead in NB register buffers (2K jobs per band, so the buffer of
+  // a job is static): NB = 2 at J = 4 (register budget), 4 below.
+  constexpr int NB = J >= 4 ? 2 : 4;
+  static_assert((2 * K) % NB == 0, "job buffers must tile a band");
+  Rows1Job<T, J> jb[NB];
+  // job jj counted from band bb's first job (jj >= 2K: the band above)
+  auto issue = [&](int bb, int jj) {
+    const int band = bb - jj / (2 * K), loc = jj % (2 * K);
+    const bool rev = loc >= K;
+    const int row = band * K + (rev ? 2 * K - 1 - loc : loc);
+    load_job<T, J>(jb[jj % NB], xg, zg, Bg, Cg, yg, row, H, W, ok && band >= 0, rev);
+  };
+#pragma unroll
+  for (int jj = 0; jj < NB - 1; ++jj) issue(nb - 1, jj);
   for (int b = nb - 1; b >= 0; --b) {
     const int r0 = b * K;
     T hp0[J];  // h of the row above the band (checkpoint / band carry / zeros)
@@ -241,12 +259,8 @@ __global__ void __launch_bounds__(128) scan2d_bwd_rows1_kernel(const Args<T> a) 
       for (int k = 0; k < J; ++k) hcur[k] = hp0[k];
 #pragma unroll
       for (int r = 0; r < K; ++r) {
-        Rows1Job<T, J>& cur = (r & 1) ? jB : jA;
-        Rows1Job<T, J>& nxt = (r & 1) ? jA : jB;
-        if (r + 1 < K)
-          load_job<T, J>(nxt, xg, zg, Bg, Cg, yg, r0 + r + 1, H, W, ok, false);
-        else
-          load_job<T, J>(nxt, xg, zg, Bg, Cg, yg, r0 + K - 1, H, W, ok, true);  // first R job
+        issue(b, r + NB - 1);
+        Rows1Job<T, J>& cur = jb[r % NB];
         T av[J], u[J];
         T hl = T(0), ap = T(1);
 #pragma unroll
@@ -273,12 +287,8 @@ __global__ void __launch_bounds__(128) scan2d_bwd_rows1_kernel(const Args<T> a) 
 #pragma unroll
     for (int rr = K - 1; rr >= 0; --rr) {
       const int jidx = K + (K - 1 - rr);  // job index within the band: K .. 2K-1
-      Rows1Job<T, J>& cur = (jidx & 1) ? jB : jA;
-      Rows1Job<T, J>& nxt = (jidx & 1) ? jA : jB;
-      if (rr > 0)
-        load_job<T, J>(nxt, xg, zg, Bg, Cg, yg, r0 + rr - 1, H, W, ok, true);
-      else
-        load_job<T, J>(nxt, xg, zg, Bg, Cg, yg, r0 - K, H, W, ok && b > 0, false);  // next band's F0
+      issue(b, jidx + NB - 1);
+      Rows1Job<T, J>& cur = jb[jidx % NB];
       const int i = r0 + rr;
       T d[J], av[J], sg[J], G[J];
       T rl = T(0), ap = T(1);  // lane aggregate of the reverse horizontal map
