@@ -250,6 +250,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--rowband", action="store_true",
                     help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), "
                          "vertical carries exchanged point to point, pipelined over scan chunks")
@@ -370,38 +371,27 @@ def main():
     extra["plan"] = op.plan()
     extra["inputs_vs_l2"] = f"inputs {fb / 1e6:.0f} MB {'>' if fb > L2_BYTES else '<='} L2 {L2_BYTES / 1e6:.0f} MB"
 
-    # ---- e2e through the C ABI from pinned host buffers
+    # ---- e2e through the C ABI with HOST operands (scan2d_train_host: the
+    #      reference call's contract -- host data in, host results out -- with the
+    #      copies pipelined against the kernels inside the library)
     e2e = None
     if not args.no_e2e:
+        from paper_2412_00678_b200.api import train_host
+
         hin = [t.cpu().pin_memory() for t in ins]
-        hdy = dy.cpu().pin_memory()
-        outs_dev = [op.y] + ([op.dx, op.dz, op.dA, op.dB, op.dC, op.dD, op.dbias] if wl["bwd"] else [])
-        hout = [torch.empty_like(t, device="cpu").pin_memory() for t in outs_dev]
-        dins = [torch.empty_like(t) for t in ins]
-        ddy = torch.empty_like(dy)
+        hdy = dy.cpu().pin_memory() if wl["bwd"] else None
+        outs = train_host(*hin, dy=hdy, chunks=args.e2e_chunks)
+        torch.cuda.synchronize()
         h2d = sum(t.numel() * t.element_size() for t in hin) + (hdy.numel() * 4 if wl["bwd"] else 0)
-        d2h = sum(t.numel() * t.element_size() for t in hout)
-
-        def e2e_step():
-            for d, h in zip(dins, hin):
-                d.copy_(h, non_blocking=True)
-            if wl["bwd"]:
-                ddy.copy_(hdy, non_blocking=True)
-            op.forward(*dins, save=wl["bwd"])
-            if wl["bwd"]:
-                op.backward(*dins, ddy)
-            for h, d in zip(hout, outs_dev):
-                h.copy_(d, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-
-        e2e_step()
+        d2h = sum(t.numel() * t.element_size() for t in outs if t is not None)
         barrier()
         k2 = max(1, args.e2e_steps)
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         ea.record(stream)
         for _ in range(k2):
-            e2e_step()
+            train_host(*hin, dy=hdy, outs=outs, chunks=args.e2e_chunks)
+            stream.synchronize()
         eb.record(stream)
         torch.cuda.synchronize()
         e_ms = ea.elapsed_time(eb) / k2
@@ -410,8 +400,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": elems / (e_ms * 1e-3) / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": k2,
-               "path": "C ABI (scan2d_forward/backward) with pinned host buffers; inputs+dy H2D, y+all grads D2H"}
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": k2, "chunks": args.e2e_chunks,
+               "path": "C ABI scan2d_train_host: pinned host operands, H2D / kernels / D2H pipelined over "
+                       "scan chunks on three streams; inputs+dy in, y+all gradients out"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -133,6 +133,23 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
                          void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip, void* dbias,
                          void* g_top, void* workspace, size_t workspace_bytes, scan2d_stream_t stream);
 
+/* ---- host operands (the reference API's contract: Grid<T> data lives in host
+ * memory, engine.hpp:88-102) ----
+ * One training step -- forward, and backward when dy != NULL -- on HOST
+ * pointers with the layouts above.  The S scans are processed in `chunks`
+ * groups through two device buffer sets: host->device copies of chunk k, the
+ * kernels of chunk k-1 and device->host copies of chunk k-2 overlap on three
+ * internal streams; `stream` is joined at both ends (call
+ * cudaStreamSynchronize(stream) before reading the outputs).  Host buffers
+ * should be page-locked (cudaHostAlloc / cudaHostRegister) for the copies to
+ * run asynchronously.  Device buffers are cached per host thread and
+ * descriptor.  Requires per-scan parameters and B/C (P == S, G == 1), else
+ * SCAN2D_EUNSUPPORTED.  With dy == NULL only y is written. */
+int scan2d_train_host(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                      const void* C, const void* A, const void* Dskip, const void* bias,
+                      const void* dy, void* y, void* dx, void* dz, void* dA, void* dB, void* dC,
+                      void* dDskip, void* dbias, int chunks, scan2d_stream_t stream);
+
 /* Typed conveniences (desc->dtype is overridden). */
 int scan2d_fwd_f32(const scan2d_desc* desc, const float* x, const float* z, const float* B,
                    const float* C, const float* A, const float* Dskip, const float* bias,

@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "scan2d_backward",
     "scan2d_forward_band",
     "scan2d_backward_band",
+    "scan2d_train_host",
     "scan2d_fwd_f32",
     "scan2d_fwd_f64",
     "scan2d_bwd_f32",
@@ -84,6 +85,8 @@ def _load():
     lib.scan2d_forward_band.restype = C.c_int
     lib.scan2d_backward_band.argtypes = [D] + [P] * 20 + [C.c_size_t, P]
     lib.scan2d_backward_band.restype = C.c_int
+    lib.scan2d_train_host.argtypes = [D] + [P] * 16 + [C.c_int, P]
+    lib.scan2d_train_host.restype = C.c_int
     for name, n_in in (("scan2d_fwd_f32", 12), ("scan2d_fwd_f64", 12)):
         getattr(lib, name).argtypes = [D] + [P] * n_in + [C.c_size_t, P]
         getattr(lib, name).restype = C.c_int

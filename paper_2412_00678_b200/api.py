@@ -360,3 +360,25 @@ class Scan2dBandOp:
             raise nat.Scan2dError(rc, "scan2d_backward_band")
         self.launches += nat.lib.scan2d_last_launch_count()
         return o.dx, o.dz, o.dA, o.dB, o.dC, o.dD, o.dbias, self.g_top
+
+
+def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 8, tile: int = 16):
+    """One training step with HOST (CPU, ideally pinned) tensors through the C
+    ABI's ``scan2d_train_host``: chunked host->device copies, kernels and
+    device->host copies overlap on three streams of the current device.
+    Returns ``outs`` = (y, dx, dz, dA, dB, dC, dD, dbias) as host tensors
+    (gradients None when ``dy`` is None).  Per-scan parameters and B/C only."""
+    S, H, W = x.shape
+    N = B.shape[-1]
+    code = nat.F64 if x.dtype == torch.float64 else nat.F32
+    desc = nat.make_desc(S, H, W, N, tile=tile, dtype=code)
+    if outs is None:
+        e = lambda *s: torch.empty(s, dtype=x.dtype).pin_memory()
+        outs = (e(S, H, W),) + ((e(S, H, W), e(S, H, W), e(S, N), e(S, H, W, N), e(S, H, W, N), e(S), e(S))
+                                if dy is not None else (None,) * 7)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rc = nat.lib.scan2d_train_host(C.byref(desc), *[_ptr(t) for t in (x, z, B, C_, A, Dskip, bias, dy)],
+                                   *[_ptr(t) for t in outs], int(chunks), _stream(dev))
+    if rc != nat.OK:
+        raise nat.Scan2dError(rc, "scan2d_train_host")
+    return outs

@@ -1,0 +1,57 @@
+"""scan2d_train_host (host operands, chunked copy/compute pipeline) against the
+device-resident path and the oracle (-m gpu)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle_lib import Oracle, rel_error
+from scan_cases import batch_to_torch, make_batch, oracle_bwd, oracle_fwd
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,chunks", [((10, 24, 40, 16), 3), ((9, 14, 14, 1), 4), ((5, 20, 32, 8), 1)])
+def test_train_host_matches_device_path(shape, chunks):
+    from paper_2412_00678_b200.api import Scan2dOp, train_host
+
+    S, H, W, N = shape
+    orc = Oracle()
+    b = make_batch(orc, S, H, W, N, seed0=900, dtype="f32")
+    (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    op = Scan2dOp(S, H, W, N, device="cuda")
+    y = op.forward(x, z, B, C, A, D, bias).clone()
+    grads = [t.clone() for t in op.backward(x, z, B, C, A, D, bias, dy)]
+    host = [t.cpu().pin_memory() for t in (x, z, B, C, A, D, bias)]
+    outs = train_host(*host, dy=dy.cpu().pin_memory(), chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], y.cpu())
+    for got, ref in zip(outs[1:], grads):
+        assert torch.equal(got, ref.cpu())
+    # and against the fp64 oracle (north_star tolerance)
+    assert rel_error(outs[0].numpy(), oracle_fwd(orc, b, "f64")) < 1e-4
+    ref = oracle_bwd(orc, b, "f64")
+    names = ["dx", "dz", "dA", "dB", "dC", "dD", "dbias"]
+    for k, got in zip(names, outs[1:]):
+        assert rel_error(got.numpy().reshape(-1), np.asarray(ref[k]).reshape(-1)) < 1e-4, k
+
+
+@pytest.mark.gpu
+def test_train_host_forward_only_and_errors():
+    from paper_2412_00678_b200 import _native as nat
+    from paper_2412_00678_b200.api import train_host
+
+    orc = Oracle()
+    b = make_batch(orc, 4, 16, 16, 4, seed0=3, dtype="f32")
+    (x, z, B, C, A, D, bias), _ = batch_to_torch(b, device="cpu")
+    outs = train_host(x, z, B, C, A, D, bias, dy=None, chunks=2)
+    torch.cuda.synchronize()
+    assert outs[1] is None
+    assert rel_error(outs[0].numpy(), oracle_fwd(orc, b, "f64")) < 1e-4
+    # shared parameters (P < S) cannot be split into scan chunks
+    import ctypes as ct
+
+    desc = nat.make_desc(4, 16, 16, 4, params_period=2)
+    ptrs = [ct.c_void_p(t.data_ptr()) for t in (x, z, B, C, A, D, bias)]
+    y = torch.empty_like(x)
+    rc = nat.lib.scan2d_train_host(ct.byref(desc), *ptrs, None, ct.c_void_p(y.data_ptr()), *([None] * 7), 2,
+                                   None)
+    assert rc == nat.EUNSUPPORTED
