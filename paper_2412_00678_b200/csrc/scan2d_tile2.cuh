@@ -623,6 +623,13 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     cp_async_commit();
   }
   T bc[CW][SH];
+  T hh0n[SH];  // saved forward carry of the next tile up
+#pragma unroll
+  for (int e = 0; e < SH; ++e) hh0n[e] = T(0);
+  {
+    const int ib = (ntiles - 1) * R + r1;
+    if (has_pred && ib < H) carry_get<T, SH>(hc_in + static_cast<size_t>(ib) * N, hh0n, SH);
+  }
 
   for (int t = ntiles - 1; t >= 0; --t) {
     const int u = ntiles - 1 - t;  // visiting index (ring phase)
@@ -643,11 +650,12 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     cp_async_commit();
     const int i1 = r0 + r1;
     const bool row_ok = r1 < rows;
-    // saved forward carry (residual), reverse carry prefetch, checkpoint row
+    // saved forward carry (residual; loaded one tile ahead), reverse carry
+    // prefetch, checkpoint row
     T hh0[SH];
 #pragma unroll
-    for (int e = 0; e < SH; ++e) hh0[e] = T(0);
-    if (has_pred && row_ok) carry_get<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh0, SH);
+    for (int e = 0; e < SH; ++e) hh0[e] = hh0n[e], hh0n[e] = T(0);
+    if (has_pred && t > 0) carry_get<T, SH>(hc_in + static_cast<size_t>(i1 - R) * N, hh0n, SH);
     CarryPre<T, SH> rpre;
     if constexpr (sizeof(T) == 4) {
       if (has_succ && !succ_ring && row_ok)
