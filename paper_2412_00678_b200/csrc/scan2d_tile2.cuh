@@ -163,6 +163,64 @@ __device__ __forceinline__ void sts_vec(T* p, const T (&v)[V]) {
   }
 }
 
+// Column-lane state vectors (SV states of one column, 16-byte units): lane
+// (j, s) visits its units in an order rotated by `rot` so that the 8 lanes of a
+// quarter-warp touch 8 distinct bank quads (fp32 N = 16: columns 2 apart alias
+// otherwise -> 2-way conflicts; N = 32: 4-way).  Register v[h*UE + k] holds
+// state s*SV + ((h + rot) % NU)*UE + k of the column.
+template <typename T, int SV>
+struct ColVec {
+  static constexpr int UE = 16 / static_cast<int>(sizeof(T)) < SV ? 16 / static_cast<int>(sizeof(T)) : SV;
+  static constexpr int NU = SV / UE;
+  int rot;
+  __device__ __forceinline__ int unit(int h) const { return NU == 1 ? 0 : (h + rot) & (NU - 1); }
+  __device__ __forceinline__ int state(int e) const { return unit(e / UE) * UE + e % UE; }
+  __device__ __forceinline__ void lds(T (&v)[SV], const T* p) const {
+#pragma unroll
+    for (int h = 0; h < NU; ++h) {
+      T t[UE];
+      lds_vec<T, UE>(t, p + unit(h) * UE);
+#pragma unroll
+      for (int k = 0; k < UE; ++k) v[h * UE + k] = t[k];
+    }
+  }
+  __device__ __forceinline__ void sts(T* p, const T (&v)[SV]) const {
+#pragma unroll
+    for (int h = 0; h < NU; ++h) {
+      T t[UE];
+#pragma unroll
+      for (int k = 0; k < UE; ++k) t[k] = v[h * UE + k];
+      sts_vec<T, UE>(p + unit(h) * UE, t);
+    }
+  }
+  __device__ __forceinline__ void ldg(T (&v)[SV], const T* p) const {
+#pragma unroll
+    for (int h = 0; h < NU; ++h) {
+      T t[UE];
+      ldg_states<T, UE>(t, p + unit(h) * UE);
+#pragma unroll
+      for (int k = 0; k < UE; ++k) v[h * UE + k] = t[k];
+    }
+  }
+  __device__ __forceinline__ void stg(T* p, const T (&v)[SV]) const {
+#pragma unroll
+    for (int h = 0; h < NU; ++h) {
+      T t[UE];
+#pragma unroll
+      for (int k = 0; k < UE; ++k) t[k] = v[h * UE + k];
+      stg_stream<T, UE>(p + unit(h) * UE, t);
+    }
+  }
+};
+
+template <typename T, int N, int SV>
+__device__ __forceinline__ ColVec<T, SV> col_vec(int j2) {
+  ColVec<T, SV> c;
+  // word offset of column j2 modulo 32 banks, in units of the lane's SV-state span
+  c.rot = sizeof(T) == 4 ? ((j2 * N) / 32) & (ColVec<T, SV>::NU - 1) : 0;
+  return c;
+}
+
 // rows r0 .. r0+R-1, columns 0 .. ncols-1 of an [H][W] plane (g already offset
 // by the strip's first column) -> [R][CW] in shared memory, 16-byte units
 template <typename TS, typename T>
@@ -368,11 +426,12 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 
   const int r1 = lane / QH, q1 = lane % QH;  // row lanes
   const int j2 = lane / QV, s2 = lane % QV;  // column lanes
+  const ColVec<T, SV> cv = col_vec<T, N, SV>(j2);
   T A1[SH], A2[SV];
 #pragma unroll
   for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
 #pragma unroll
-  for (int e = 0; e < SV; ++e) A2[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + e]);
+  for (int e = 0; e < SV; ++e) A2[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + cv.state(e)]);
 
   for (int e = lane; e < TS::F_TOTAL; e += 32) sm[e] = T(0);
   __syncwarp();
@@ -397,7 +456,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   T hv[SV];  // vertical state: zeros, or the row above the band (row-band shard)
 #pragma unroll
   for (int e = 0; e < SV; ++e) hv[e] = T(0);
-  if (a.vtop != nullptr && col_ok) ldg_states<T, SV>(hv, a.vtop + (s * W + jg2) * N + s2 * SV);
+  if (a.vtop != nullptr && col_ok) cv.ldg(hv, a.vtop + (s * W + jg2) * N + s2 * SV);
 
   const int ntiles = (H + R - 1) / R;
   int sc = 0;  // slot holding this tile's C; sc+1: hh of this tile; sc+2: C of the next tile
@@ -499,8 +558,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
       for (int r = 0; r < R; ++r) {
         const T dj = Ds[r * CW + j2];
         T h4[SV], c4[SV];
-        lds_vec<T, SV>(h4, hcol + r * BP);
-        lds_vec<T, SV>(c4, ccol + r * BP);
+        cv.lds(h4, hcol + r * BP);
+        cv.lds(c4, ccol + r * BP);
         T acc0 = T(0), acc1 = T(0);
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
@@ -518,10 +577,10 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
           if (s2 == 0) __stcs(yp + static_cast<size_t>(r) * W, fma(Dsk, Xs[r * CW + j2], acc));
           if (save && r == R - 1 && i < H - 1) {  // checkpoint: h at the last row of every tile
             T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + t) * W + jg2) * N + s2 * SV;
-            stg_states<T, SV>(ck, hv, SV, true);
+            cv.stg(ck, hv);
           }
           if (i == H - 1 && a.vbot != nullptr)  // row-band shard: the next band's vtop
-            stg_states<T, SV>(a.vbot + (s * W + jg2) * N + s2 * SV, hv, SV, true);
+            cv.stg(a.vbot + (s * W + jg2) * N + s2 * SV, hv);
         }
       }
     }
@@ -566,6 +625,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
 
   const int r1 = lane / QH, q1 = lane % QH;
   const int j2 = lane / QV, s2 = lane % QV;
+  const ColVec<T, SV> cv = col_vec<T, N, SV>(j2);
   T A1[SH];
 #pragma unroll
   for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
@@ -605,7 +665,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
   T dn[SV];  // Abar(i+1,j) G(i+1,j), carried up across tiles (column lanes)
 #pragma unroll
   for (int e = 0; e < SV; ++e) dn[e] = T(0);
-  if (a.gbot != nullptr && col_ok) ldg_states<T, SV>(dn, a.gbot + (s * W + jg2) * N + s2 * SV);
+  if (a.gbot != nullptr && col_ok) cv.ldg(dn, a.gbot + (s * W + jg2) * N + s2 * SV);
   T dAr[SH];
 #pragma unroll
   for (int e = 0; e < SH; ++e) dAr[e] = T(0);
@@ -667,9 +727,9 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     for (int e = 0; e < SV; ++e) hp0[e] = T(0);
     if (t > 0 && col_ok) {
       const T* ck = a.ckpt + ((static_cast<size_t>(s) * nbm1 + (t - 1)) * W + jg2) * N + s2 * SV;
-      ldg_states<T, SV>(hp0, ck);
+      cv.ldg(hp0, ck);
     } else if (a.vtop != nullptr && col_ok) {  // row-band shard: h of the row above the band
-      ldg_states<T, SV>(hp0, a.vtop + (s * W + jg2) * N + s2 * SV);
+      cv.ldg(hp0, a.vtop + (s * W + jg2) * N + s2 * SV);
     }
     cp_async_wait<1>();
     __syncwarp();
@@ -697,19 +757,19 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     {
       T* gcol = Cs + j2 * N + s2 * SV;
       T A2[SV];
-      lds_vec<T, SV>(A2, As + s2 * SV);
+      cv.lds(A2, As + s2 * SV);
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
         const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
         T g4[SV];
-        lds_vec<T, SV>(g4, gcol + r * BP);
+        cv.lds(g4, gcol + r * BP);
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
           const T g = fma(g4[e], dyv, dn[e]);
           dn[e] = Num<T>::exp_scaled(dj * A2[e]) * g;
           g4[e] = g;
         }
-        if (col_ok) sts_vec<T, SV>(gcol + r * BP, g4);
+        if (col_ok) cv.sts(gcol + r * BP, g4);
       }
     }
     // ---- F1 (row lanes): hh left -> right from the saved carry
@@ -742,15 +802,15 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
       const T* hcol = HHs + j2 * N + s2 * SV;
       const T* gcol = Cs + j2 * N + s2 * SV;
       T hcur[SV], A2[SV], dAc[SV];
-      lds_vec<T, SV>(A2, As + s2 * SV);
+      cv.lds(A2, As + s2 * SV);
 #pragma unroll
       for (int e = 0; e < SV; ++e) hcur[e] = hp0[e], dAc[e] = T(0);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const T dj = Ds[r * CW + j2], dyv = Ys[r * CW + j2];
         T h4[SV], g4[SV];
-        lds_vec<T, SV>(h4, hcol + r * BP);
-        lds_vec<T, SV>(g4, gcol + r * BP);
+        cv.lds(h4, hcol + r * BP);
+        cv.lds(g4, gcol + r * BP);
         T ddv = T(0);
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
@@ -767,7 +827,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
           T dc[SV];
 #pragma unroll
           for (int e = 0; e < SV; ++e) dc[e] = dyv * hcur[e];
-          stg_stream<T, SV>(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
+          cv.stg(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
         }
       }
       T acc[SV];
@@ -858,7 +918,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
   }
 
   if (a.gtop != nullptr && col_ok)  // row-band shard: the band above continues from here
-    stg_states<T, SV>(a.gtop + (s * W + jg2) * N + s2 * SV, dn, SV, true);
+    cv.stg(a.gtop + (s * W + jg2) * N + s2 * SV, dn);
 
   // ---- per-(scan, strip) partials, fixed order: dA = row-lane part + column-lane part
 #pragma unroll
@@ -882,7 +942,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
   T* part = a.part + (static_cast<size_t>(s) * ge.wreal + wpos) * (N + 2);
   if (lane < QV) {
 #pragma unroll
-    for (int e = 0; e < SV; ++e) part[s2 * SV + e] = scr[s2 * SV + e] + dAc[e];
+    for (int e = 0; e < SV; ++e) part[s2 * SV + cv.state(e)] = scr[s2 * SV + cv.state(e)] + dAc[e];
   }
   if (lane == 0) {
     part[N] = dbias_acc;
