@@ -830,11 +830,11 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
           cv.stg(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
         }
       }
-      T acc[SV];
-      lds_vec<T, SV>(acc, DAs);
+      T acc[SV];  // DAs holds the lane's dA partials in natural state order
+      cv.lds(acc, DAs);
 #pragma unroll
       for (int e = 0; e < SV; ++e) acc[e] += dAc[e];
-      sts_vec<T, SV>(DAs, acc);
+      cv.sts(DAs, acc);
     }
     __syncwarp();
 
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
   T* part = a.part + (static_cast<size_t>(s) * ge.wreal + wpos) * (N + 2);
   if (lane < QV) {
 #pragma unroll
-    for (int e = 0; e < SV; ++e) part[s2 * SV + cv.state(e)] = scr[s2 * SV + cv.state(e)] + dAc[e];
+    for (int e = 0; e < SV; ++e) part[s2 * SV + e] = scr[s2 * SV + e] + dAc[e];
   }
   if (lane == 0) {
     part[N] = dbias_acc;

@@ -1,6 +1,6 @@
 # bench lines (no cpu/e2e) for WLS under each VARIANTS entry (A=B[,C=D] or base)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2 > gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2 > gpurun_out/pytest_gpu.log; grep -q failed gpurun_out/pytest_gpu.log && echo "!!!!!!!! PYTEST FAILED !!!!!!!!"
 : > gpurun_out/bench_var.jsonl
 for v in ${VARIANTS:-base}; do
   for w in ${WLS:-cfg2 cfg3}; do
