@@ -140,7 +140,8 @@ int tile_sh(const scan2d_desc& d) {
 // checkpointed every 4 rows.  The warp kernels (reference CarryState emission)
 // accept the same residual layout.
 bool rows1_shape(const scan2d_desc& d) {
-  return d.state_dim == 1 && d.width <= 128 && env_int("SCAN2D_ROWS1", 1) == 1;
+  const int wmax = d.dtype == SCAN2D_F64 ? 64 : 128;  // 32 lanes x 16 bytes
+  return d.state_dim == 1 && d.width <= wmax && env_int("SCAN2D_ROWS1", 1) == 1;
 }
 
 int make_plan(const scan2d_desc& d, Plan& p) {
@@ -152,7 +153,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
     p.Q = d.width;
     p.nq = 0;
-    if (p.f.wreal > 1 || p.b.wreal > 1) return SCAN2D_EUNSUPPORTED;  // cannot happen for W <= 128
+    p.warp_ok = p.f.wreal == 1 && p.b.wreal == 1;  // W <= 128 (fp32) / 64 (fp64): always
     return SCAN2D_OK;
   }
   p.K = std::min(env_int("SCAN2D_BAND_ROWS", 8), static_cast<int>(d.height));
@@ -167,14 +168,20 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     // checkpoints every backward tile (R = 32 * SH / N rows)
     p.K = std::min(32 * tile_sh(d) / N, static_cast<int>(d.height));
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
-    while (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0 && p.b.J < 4) {
-      p.b.J *= 2;
-      p.b.colsw = p.b.cps * p.b.J;
-      p.b.wreal = static_cast<int>(ceil_div(d.width, p.b.colsw));
-      p.b.units = ceil_div(d.num_scans, p.b.seg) * p.b.wreal;
-    }
-    if (p.b.wreal > 1 && (p.b.colsw % p.Q) != 0) return SCAN2D_EUNSUPPORTED;
-    if ((p.Q % p.f.J) != 0 || (p.f.wreal > 1 && (p.f.colsw % p.Q) != 0)) return SCAN2D_EUNSUPPORTED;
+    // the warp kernels (fallback for unaligned operands, CarryState emission)
+    // must put their column-group boundaries on the same 16-column grid
+    auto widen = [&](s2d::Geo& g, int jmax) {
+      while (g.wreal > 1 && (g.colsw % p.Q) != 0 && g.J < jmax) {
+        g.J *= 2;
+        g.colsw = g.cps * g.J;
+        g.wreal = static_cast<int>(ceil_div(d.width, g.colsw));
+        g.units = ceil_div(d.num_scans, g.seg) * g.wreal;
+      }
+    };
+    widen(p.b, 4);
+    widen(p.f, 8);
+    p.warp_ok = !(p.b.wreal > 1 && (p.b.colsw % p.Q) != 0) &&
+                !((p.Q % p.f.J) != 0 || (p.f.wreal > 1 && (p.f.colsw % p.Q) != 0));
     return SCAN2D_OK;
   }
   if (p.b.wreal > 1) {
@@ -191,6 +198,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
     p.Q = p.f.colsw;
     p.nq = static_cast<int>(ceil_div(d.width, p.Q)) - 1;
   }
+  p.warp_ok = 1;
   return SCAN2D_OK;
 }
 
@@ -227,10 +235,11 @@ bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec, bool emit) {
 // the backward J = 4 (more work per lane between its shuffle scans).
 bool rows1_geo(s2d::Geo& g, const scan2d_desc& d, int align_bytes, bool bwd) {
   const int es = static_cast<int>(dtype_size(d.dtype));
-  const int jmax = env_int(bwd ? "SCAN2D_ROWS1_JB" : "SCAN2D_ROWS1_JF", bwd ? 4 : 2);
+  // preferred J first; wider / narrower ones when the width or alignment needs it
+  const int pref = env_int(bwd ? "SCAN2D_ROWS1_JB" : "SCAN2D_ROWS1_JF", bwd ? 4 : 2);
+  const int order[3] = {pref, pref == 4 ? 2 : 4, 1};
   int J = 0;
-  for (int j : {4, 2, 1}) {
-    if (j > jmax) continue;
+  for (int j : order) {
     if (d.width % j == 0 && j * es <= 16 && align_bytes % (j * es) == 0 && d.width / j <= 32) {
       J = j;
       break;
@@ -310,8 +319,10 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool em
       if (eb < 0 || b.smem_bytes > 200 * 1024) return SCAN2D_EUNSUPPORTED;
       return SCAN2D_OK;
     }
+    if (!p.warp_ok) return SCAN2D_EUNSUPPORTED;
     return finish_geo(p.b, d, true, p.K, xvec, bvec);
   }
+  if (!p.warp_ok) return SCAN2D_EUNSUPPORTED;
   rc = finish_geo(p.f, d, false, p.K, xvec, bvec);
   if (rc != SCAN2D_OK) return rc;
   return finish_geo(p.b, d, true, p.K, xvec, bvec);

@@ -426,6 +426,7 @@ struct Plan {
   int nb;     // ceil(H / K)
   int Q;      // column interval of the saved horizontal carries (= b.colsw)
   int nq;     // ceil(W / Q) - 1 carry boundaries per row
+  int warp_ok;  // the warp kernels' geometry fits this residual layout (else tile / rows1 kernels only)
 };
 
 template <typename T>

@@ -1,0 +1,74 @@
+"""Parity of every kernel family the planner can pick, forward and backward,
+against the fp64 oracle (-m gpu):
+  * tile kernels (scan2d_tile2.cuh): N in {4, 8, 16, 32}, fp32 (SH = 2) and
+    fp64 (SH = 1); partial tiles (H not a multiple of the tile height),
+    partial strips, one CTA per scan and several CTAs chained through global
+    carries (> 13 strips);
+  * N = 1 row-sweep kernels (scan2d_rows1.cuh): J in {4, 2, 1} columns per
+    lane, 8/16/32-lane segments, odd widths that fall back to the warp
+    kernels;
+  * the plan actually taken is checked, so a silent fallback cannot pass.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle_lib import Oracle, rel_error
+from scan_cases import batch_to_torch, make_batch, oracle_bwd, oracle_fwd
+
+F32_GATE = 1e-4
+F64_Y_GATE = 1e-12
+F64_G_GATE = 1e-10
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def _run(orc, S, H, W, N, dtype, seed):
+    from paper_2412_00678_b200.api import Scan2dOp
+
+    b = make_batch(orc, S, H, W, N, seed0=seed, dtype=dtype)
+    (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    op = Scan2dOp(S, H, W, N, dtype=x.dtype, device="cuda")
+    y = op.forward(x, z, B, C, A, D, bias).clone()
+    grads = [t.clone() for t in op.backward(x, z, B, C, A, D, bias, dy)]
+    torch.cuda.synchronize()
+    return b, op, y, grads
+
+
+def _check(orc, b, y, grads, dtype, label):
+    yg, gg = (F64_Y_GATE, F64_G_GATE) if dtype == "f64" else (F32_GATE, F32_GATE)
+    e = rel_error(y.cpu().numpy(), oracle_fwd(orc, b, "f64"))
+    assert e <= yg, f"{label}: y rel {e:.3e}"
+    ref = oracle_bwd(orc, b, "f64")
+    for k, t in zip(("dx", "dz", "dA", "dB", "dC", "dD", "dbias"), grads):
+        e = rel_error(t.cpu().numpy().reshape(-1), np.asarray(ref[k]).reshape(-1))
+        assert e <= gg, f"{label}: {k} rel {e:.3e}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [4, 8, 16, 32])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("H,W", [(37, 40), (9, 212), (5, 16)])
+def test_tile_kernels(orc, N, dtype, H, W):
+    S = 3
+    b, op, y, grads = _run(orc, S, H, W, N, dtype, seed=77 + N + H)
+    plan = op.plan()
+    assert plan["cols_per_chunk"] == 1 and plan["cols_per_warp"] == 16, plan  # tile kernels ran
+    _check(orc, b, y, grads, dtype, f"tile N={N} {dtype} {H}x{W}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [4, 7, 12, 14, 28, 30, 56, 64, 100, 128, 33])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_rows1_kernels(orc, W, dtype):
+    S, H = 9, 13
+    b, op, y, grads = _run(orc, S, H, W, 1, dtype, seed=300 + W)
+    plan = op.plan()
+    if W == 33 or (dtype == "f64" and W > 64):  # no J puts the row on <= 32 lanes: warp kernels
+        assert plan["spl_x100_plus_lpc"] != 0, plan
+    else:
+        assert plan["spl_x100_plus_lpc"] == 0 and plan["cols_per_warp"] == W, plan  # row-sweep kernels ran
+    _check(orc, b, y, grads, dtype, f"rows1 W={W} {dtype}")
