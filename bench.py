@@ -250,7 +250,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--e2e-chunks", type=int, default=0, help="0 = library heuristic")
     ap.add_argument("--rowband", action="store_true",
                     help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), "
                          "vertical carries exchanged point to point, pipelined over scan chunks")

@@ -144,7 +144,8 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
  * should be page-locked (cudaHostAlloc / cudaHostRegister) for the copies to
  * run asynchronously.  Device buffers are cached per host thread and
  * descriptor.  Requires per-scan parameters and B/C (P == S, G == 1), else
- * SCAN2D_EUNSUPPORTED.  With dy == NULL only y is written. */
+ * SCAN2D_EUNSUPPORTED.  With dy == NULL only y is written.  chunks <= 0 picks
+ * the count automatically (>= 32 MB of input per chunk, at most 8). */
 int scan2d_train_host(const scan2d_desc* desc, const void* x, const void* z, const void* B,
                       const void* C, const void* A, const void* Dskip, const void* bias,
                       const void* dy, void* y, void* dx, void* dz, void* dA, void* dB, void* dC,

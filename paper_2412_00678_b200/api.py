@@ -362,7 +362,7 @@ class Scan2dBandOp:
         return o.dx, o.dz, o.dA, o.dB, o.dC, o.dD, o.dbias, self.g_top
 
 
-def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 8, tile: int = 16):
+def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 0, tile: int = 16):
     """One training step with HOST (CPU, ideally pinned) tensors through the C
     ABI's ``scan2d_train_host``: chunked host->device copies, kernels and
     device->host copies overlap on three streams of the current device.

@@ -133,7 +133,13 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
   if (!x || !z || !B || !C || !A || !Dskip || !bias || !y) return SCAN2D_EINVAL;
   const bool bwd = dy != nullptr;
   if (bwd && (!dx || !dz || !dA || !dB || !dC || !dDskip || !dbias)) return SCAN2D_EINVAL;
-  if (chunks < 1) chunks = 1;
+  if (chunks < 1) {  // auto: >= 32 MB of host->device traffic per chunk, at most 8 chunks
+    size_t in[8], out[8];
+    counts(d, d.num_scans, in, out);
+    size_t bytes = 0;
+    for (int i = 0; i < 8; ++i) bytes += in[i] * es_of(d.dtype);
+    chunks = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, bytes / (32u << 20))));
+  }
   if (chunks > d.num_scans) chunks = static_cast<int>(d.num_scans);
   // chunks split scans, so parameters and B/C must be per scan
   if (d.params_period != d.num_scans || d.bc_group != 1) return SCAN2D_EUNSUPPORTED;
