@@ -115,6 +115,16 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
   }
 }
 
+// Pause between polls of a carry word.  __nanosleep deschedules the warp for
+// far longer than asked on sm_100 when the word is not ready yet (one global
+// hop between two CTAs measured 2.2x slower with it); a short clock spin keeps
+// the re-poll latency near the L2 round trip.
+__device__ __forceinline__ void poll_pause() {
+  const long long t0 = clock64();
+  while (clock64() - t0 < 64) {
+  }
+}
+
 // ------------------------------------------------------ gpu-scope carries
 //
 // Tags are unique per (launch, row): the host advances `epoch` by H + 1 per
@@ -144,7 +154,7 @@ struct CarrySlot<float> {
     uint64_t w;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(&p->w) : "memory");
     while (static_cast<int>(w >> 32) != tag) {
-      __nanosleep(64);
+      poll_pause();
       asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(&p->w) : "memory");
     }
     return __uint_as_float(static_cast<uint32_t>(w));
@@ -168,7 +178,7 @@ struct CarrySlot<double> {
     long long t;
     asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(t) : "l"(&p->tag) : "memory");
     while (static_cast<int>(t) != tag) {
-      __nanosleep(20);
+      poll_pause();
       asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(t) : "l"(&p->tag) : "memory");
     }
     double v;
@@ -206,7 +216,7 @@ __device__ __forceinline__ void carry_get_wait(const CarrySlot<T>* p, T (&v)[SPL
       bool ok;
       int spins = 0;
       do {
-        if (spins++) __nanosleep(64);
+        if (spins++) poll_pause();
 #pragma unroll
         for (int e = 0; e < SPL; e += 2)
           asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
@@ -254,7 +264,7 @@ __device__ __forceinline__ void carry_resolve(const CarrySlot<float>* p, CarryPr
 #pragma unroll
   for (int e = 0; e < SPL; ++e) ok = ok && static_cast<int>(c.w[e] >> 32) == tag;
   while (!ok) {
-    __nanosleep(64);
+    poll_pause();
     carry_load<SPL>(p, c);
     ok = true;
 #pragma unroll
