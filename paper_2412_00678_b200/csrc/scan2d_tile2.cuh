@@ -311,9 +311,11 @@ __device__ __forceinline__ void prefetch_tile(const T* g, int r0, int H, size_t 
 // words, and CTAs take tickets so a producer CTA is always resident first.
 
 constexpr int kRing = 4;  // carry ring depth (tiles)
-// warps (strips) per CTA at most: 13 x 32 threads x 152 registers fit one SM's
-// register file, and 13 strips cover a 200-column grid in one CTA
+// warps (strips) per CTA at most.  Forward: 13 (128 registers, 13 strips = a
+// 200-column scan per CTA).  Backward: 12 = 3 per SM sub-partition, so up to
+// 168 registers per thread (no spills).
 constexpr int kTileMaxWarps = 13;
+constexpr int kTileMaxWarpsBwd = 12;
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -368,29 +370,38 @@ struct CarryRing {
   }
 };
 
-// CTA ticket + strip identity.  rev: strips of a scan are taken right to left
-// (backward).  Returns false for warps past the scan's last strip.
+// CTA ticket + strip identity.  The S x wreal strips are numbered scan-major
+// and dealt to CTAs in contiguous runs of nw (one warp each), so a CTA may end
+// one scan and start the next: every SM gets an equal share of strips (139 of
+// the 148 SMs busy for 128 scans x 13 strips instead of 128).  Consecutive
+// warps of one scan pass the carry through the shared-memory ring; the first /
+// last warp of a run uses the tagged global words.  CTAs take tickets so the
+// CTA holding a strip's producer is always resident first.  rev (backward):
+// strips are dealt right to left, so warp wi+1 holds the LEFT neighbour.
 struct StripId {
   int64_t s;
-  int strip, wi, nw, cpos, ncta;
+  int strip, wi, nw;
+  bool valid;
 };
 
-__device__ __forceinline__ StripId strip_id(const Geo& ge, int* ticket, bool rev) {
+__device__ __forceinline__ StripId strip_id(const Geo& ge, int64_t S, int* ticket, bool rev) {
   __shared__ int tk;
   StripId id;
   id.nw = blockDim.x / 32;
   id.wi = threadIdx.x / 32;
-  id.ncta = ge.ctas_per_scan;
   int64_t unit = blockIdx.x;
-  if (id.ncta > 1) {
+  if (ge.wreal > 1) {
     if (threadIdx.x == 0) tk = atomicAdd(ticket, 1);
     __syncthreads();
     unit = tk;
   }
-  id.s = unit / id.ncta;
-  id.cpos = static_cast<int>(unit % id.ncta);
-  if (rev) id.cpos = id.ncta - 1 - id.cpos;
-  id.strip = id.cpos * id.nw + id.wi;
+  const int64_t total = S * ge.wreal;
+  int64_t g = unit * id.nw + id.wi;
+  id.valid = g < total;
+  if (rev) g = total - 1 - g;
+  if (!id.valid) g = 0;
+  id.s = g / ge.wreal;
+  id.strip = static_cast<int>(g % ge.wreal);
   return id;
 }
 
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   constexpr uint32_t ES = sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& ge = a.plan.f;
-  const StripId id = strip_id(ge, a.ticket, false);
+  const StripId id = strip_id(ge, a.S, a.ticket, false);
   const int lane = threadIdx.x & 31;
   CarryRing<T, SH> ring;
   ring.setup(smem_raw + static_cast<size_t>(id.nw) * TS::F_TOTAL * ES, id.nw);
@@ -412,7 +423,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
     mbar_init(ring.empty + threadIdx.x, 32);
   }
   __syncthreads();
-  if (id.strip >= ge.wreal) return;
+  if (!id.valid) return;
   T* sm = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(id.wi) * TS::F_TOTAL;
   const int H = a.H, W = a.W;
   const int64_t s = id.s;
@@ -594,14 +605,14 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 // CW = 16: up to 13 warps (128 registers); CW = 32 (fp32, N <= 16): up to 8
 // warps with the register room for 32-column strips (7 strips cover 200 columns)
 template <typename T, int N, int CW, int SH>
-__global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
+__global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
   using TS = T2Shape<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
   constexpr int RG = TS::RG;
   constexpr uint32_t ES = sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& ge = a.plan.b;
-  const StripId id = strip_id(ge, a.ticket, true);
+  const StripId id = strip_id(ge, a.S, a.ticket, true);
   const int lane = threadIdx.x & 31;
   CarryRing<T, SH> ring;
   ring.setup(smem_raw + static_cast<size_t>(id.nw) * TS::B_TOTAL * ES, id.nw);
@@ -610,7 +621,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
     mbar_init(ring.empty + threadIdx.x, 32);
   }
   __syncthreads();
-  if (id.strip >= ge.wreal) return;
+  if (!id.valid) return;
   T* sm = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(id.wi) * TS::B_TOTAL;
   const int H = a.H, W = a.W;
   const int64_t s = id.s;
@@ -647,9 +658,10 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
 
   const int nq = a.plan.nq, nbm1 = a.plan.nb - 1;
   const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
-  // reverse carry: from the warp on the right (ring) or across the CTA boundary (global)
-  const bool succ_ring = has_succ && id.wi + 1 < id.nw;
-  const bool pred_ring = has_pred && id.wi > 0;
+  // reverse carry: from the warp on the right (warp wi-1, ring) or across the
+  // CTA boundary (global); to the warp on the left (warp wi+1)
+  const bool succ_ring = has_succ && id.wi > 0;
+  const bool pred_ring = has_pred && id.wi + 1 < id.nw;
   // saved forward carries sit on the forward's 16-column grid (plan.Q)
   const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (c0 / a.plan.Q - 1)) * H) * N + q1 * SH : nullptr;
   const int wb = ge.wreal - 1;
@@ -844,7 +856,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
 #pragma unroll
       for (int e = 0; e < SH; ++e) rho[e] = T(0);
       if (succ_ring) {
-        ring.get(id.wi, u, lane, rho);
+        ring.get(id.wi - 1, u, lane, rho);
         if (!row_ok) {
 #pragma unroll
           for (int e = 0; e < SH; ++e) rho[e] = T(0);
@@ -909,7 +921,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarps : 256, 1) scan2d
         }
       }
       if (pred_ring)
-        ring.put(id.wi - 1, u, lane, rho);
+        ring.put(id.wi, u, lane, rho);
       else if (has_pred && row_ok)
         carry_put<T, SH>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
     }
