@@ -695,6 +695,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     cp_async_commit();
   }
   T bc[CW][SH];
+  load_b_rows<T, CW, SH>(bc, Bg, (ntiles - 1) * R + r1, H, WN, ncols, N);
   T hh0n[SH];  // saved forward carry of the next tile up
 #pragma unroll
   for (int e = 0; e < SH; ++e) hh0n[e] = T(0);
@@ -709,9 +710,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     const int rows = min(R, H - r0);
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
-    // this tile's B operand (row lanes) first: registers allow no second set, so
-    // its latency is covered by the copies, the per-cell prologue and phase CA
-    load_b_rows<T, CW, SH>(bc, Bg, r0 + r1, H, WN, ncols, N);
+    // this tile's B operand (row lanes) was loaded column by column as the
+    // previous tile's R2 finished with each column (one register set only)
     if (t > 0) {
       const int ru = r0 - R;
       issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
@@ -904,6 +904,15 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           ddp[jj] = dd;
           sgb[jj] = sg;
           if (row_ok && j < ncols) stg_stream<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
+        }
+        // columns gs .. gs+RG-1 are done with B: load the next tile's (one up) in place
+        if (t > 0) {
+#pragma unroll
+          for (int jj = 0; jj < RG; ++jj) {
+            const int j = gs + jj;
+            if (j < ncols)
+              ldg_states<T, SH>(bc[j], Bg + static_cast<size_t>(i1 - R) * WN + static_cast<size_t>(j) * N);
+          }
         }
         const int cb = reduce_scatter<QH, RG>(ddp, q1);
         reduce_scatter<QH, RG>(sgb, q1);
