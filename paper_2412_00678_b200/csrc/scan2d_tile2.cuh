@@ -549,6 +549,9 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 #pragma unroll
           for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
           if (j < ncols) sts_vec<T, SH>(hr + j * N, hh);
+          // column j is done with B: load the next tile's in place
+          if (t + 1 < ntiles && j < ncols && i1 + R < H)
+            ldg_states<T, SH>(bc[j], Bg + static_cast<size_t>(i1 + R) * WN + static_cast<size_t>(j) * N);
         }
       }
       // strips other than the last are full (ncols == CW): hh is the boundary carry
@@ -556,7 +559,6 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
       if (has_succ && row_ok && (save || !succ_ring))
         carry_put<T, SH>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
     }
-    if (t + 1 < ntiles) load_b_rows<T, CW, SH>(bc, Bg, r0 + R + r1, H, WN, ncols, N);
     __syncwarp();
 
     // ---- phase 2 (column lanes): h top -> down, y = D x + sum_d C h
