@@ -44,7 +44,7 @@ int check_desc(const scan2d_desc* d) {
   if (d->bc_group < 1 || d->num_scans % d->bc_group != 0) return SCAN2D_EINVAL;
   if (d->dtype != SCAN2D_F32 && d->dtype != SCAN2D_F64) return SCAN2D_EINVAL;
   if (d->reserved != 0) return SCAN2D_EINVAL;
-  if (d->state_dim > 32) return SCAN2D_EUNSUPPORTED;  // state groups > 32: not yet
+  if (d->state_dim > 128) return SCAN2D_EUNSUPPORTED;  // one warp spans <= 128 states (32 lanes x 4)
   return SCAN2D_OK;
 }
 

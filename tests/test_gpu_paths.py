@@ -72,3 +72,14 @@ def test_rows1_kernels(orc, W, dtype):
     else:
         assert plan["spl_x100_plus_lpc"] == 0 and plan["cols_per_warp"] == W, plan  # row-sweep kernels ran
     _check(orc, b, y, grads, dtype, f"rows1 W={W} {dtype}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,W", [(33, 21), (48, 21), (64, 21), (100, 21), (128, 21), (64, 300), (128, 130)])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_wide_state_warp_kernels(orc, N, W, dtype):
+    """N in (32, 128]: the general warp kernels (up to 4 states x 32 lanes per chunk),
+    single and chained column groups."""
+    S, H = 2, 11
+    b, op, y, grads = _run(orc, S, H, W, N, dtype, seed=500 + N)
+    _check(orc, b, y, grads, dtype, f"warp N={N} {dtype}")
