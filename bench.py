@@ -230,10 +230,37 @@ class CpuReference:
                            f"best of {reps}; one scan single-threaded {self.t1 * 1e3:.2f} ms")}
 
 
-def cpu_reference(wl, target_s=10.0, reps=3):
+def cpu_reference(wl, target_s=10.0, reps=3, parity_dev=None):
     cr = CpuReference(wl, target_s)
     best = min(cr.step() for _ in range(reps))
-    return cr.describe(best, reps)
+    out = cr.describe(best, reps)
+    if parity_dev is not None and cr.ref is not None:
+        out["parity"] = parity_vs_reference(cr, parity_dev)
+    return out
+
+
+def parity_vs_reference(cr, dev, max_scans=16):
+    """North_star parity report: y of the GPU path vs the reference library's
+    fp64 engine on the CPU sample's own inputs (normwise error of
+    test_util.hpp:17-26 and the per-element distribution)."""
+    import numpy as np
+    import torch
+
+    from oracle_lib import elem_stats, rel_error
+    from paper_2412_00678_b200.api import Scan2dOp
+
+    wl = cr.wl
+    k = min(cr.k, max_scans)
+    H, W, N = wl["H"], wl["W"], wl["N"]
+    x, z, B, C, A, D, bias, _ = [a[:k] for a in cr.arrs]
+    _, y64 = cr.ref.batch(k, k, 1, H, W, N, 16, cr.threads, False,
+                          *[np.asarray(v, np.float64) for v in (x, z, B, C, A, D, bias)], dtype="f64",
+                          want_y=True)
+    t = [torch.from_numpy(np.ascontiguousarray(v)).to(dev) for v in (x, z, B, C, A, D, bias)]
+    op = Scan2dOp(k, H, W, N, tile=16, device=dev, with_backward=False)
+    y = op.forward(*t, save=False).cpu().numpy()
+    return {"scans": k, "against": "reference tiled_scan_2d_forward<double> (oracle/_ref)",
+            "normwise_rel": rel_error(y, y64), "tolerance": 1e-4, "elem_rel": elem_stats(y, y64)}
 
 
 # ----------------------------------------------------------------- main
@@ -360,7 +387,7 @@ def main():
         dom_name, dom_bytes, dom_ms = ("scan2d_fwd_tile2_kernel" if tile else "scan2d_fwd_kernel"), fb, fwd_ms
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_source": peak_src,
+            "frac": achieved / peak, "peak_source": peak_src, "frac_of_nominal_8000": achieved / 8000.0,
             "traffic": traffic.get(dom_name, {}).get("dram_bytes_per_launch"),
             "algorithmic_bytes_per_launch": dom_bytes,
             "launch_ms": dom_ms}
@@ -369,6 +396,7 @@ def main():
         extra.update({"bwd_ms": bwd_ms, "bwd_gbs": bb / (bwd_ms * 1e-3) / 1e9,
                       "bwd_frac": bb / (bwd_ms * 1e-3) / 1e9 / peak})
     extra["plan"] = op.plan()
+    extra["gstate_updates_per_s"] = value * wl["N"]
     extra["inputs_vs_l2"] = f"inputs {fb / 1e6:.0f} MB {'>' if fb > L2_BYTES else '<='} L2 {L2_BYTES / 1e6:.0f} MB"
 
     # ---- e2e through the C ABI with HOST operands (scan2d_train_host: the
@@ -407,7 +435,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference(wl)
+            cpu = cpu_reference(wl, parity_dev=dev)
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "Gelem/s", "cores": 0, "kind": "unavailable", "sample": str(exc)}
 
