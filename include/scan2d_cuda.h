@@ -52,7 +52,7 @@ extern "C" {
 #define SCAN2D_ESTALE 2        /* no valid saved forward  (std::logic_error)      */
 #define SCAN2D_ECUDA 3         /* CUDA launch / runtime error                     */
 #define SCAN2D_ENOMEM 4        /* workspace too small                             */
-#define SCAN2D_EUNSUPPORTED 5  /* device is not sm_100, or N > 128                 */
+#define SCAN2D_EUNSUPPORTED 5  /* device is not sm_100 / configuration not served  */
 
 #define SCAN2D_F32 0
 #define SCAN2D_F64 1
@@ -69,7 +69,7 @@ typedef struct scan2d_desc {
   int64_t num_scans;    /* S >= 1                                              */
   int32_t height;       /* H >= 1                                              */
   int32_t width;        /* W >= 1                                              */
-  int32_t state_dim;    /* N in [1, 2048]; this library runs N <= 128          */
+  int32_t state_dim;    /* N in [1, 2048] (N > 128: passes over state groups)  */
   int32_t tile;         /* reference TileConfig T >= 1 (layout of ph / pv)     */
   int32_t params_period;/* P >= 1, divides S                                    */
   int32_t bc_group;     /* G >= 1, divides S                                    */

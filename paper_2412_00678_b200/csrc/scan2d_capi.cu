@@ -18,6 +18,18 @@
 using s2d::Args;
 using s2d::Plan;
 
+// scan2d_groups.cu: state dimensions above 128 as passes over state groups
+size_t scan2d_groups_workspace_bytes(const scan2d_desc& d, int op);
+size_t scan2d_groups_residual_bytes(const scan2d_desc& d);
+int scan2d_groups_forward(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
+                          const void* A, const void* Dskip, const void* bias, void* y, void* ph, void* pv,
+                          void* residual, void* ws, size_t ws_bytes, cudaStream_t st);
+int scan2d_groups_backward(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
+                           const void* A, const void* Dskip, const void* bias, const void* residual,
+                           const void* dy, void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip,
+                           void* dbias, void* ws, size_t ws_bytes, cudaStream_t st);
+constexpr int kMaxKernelN = 128;
+
 namespace {
 
 thread_local int g_last_launches = 0;
@@ -44,7 +56,7 @@ int check_desc(const scan2d_desc* d) {
   if (d->bc_group < 1 || d->num_scans % d->bc_group != 0) return SCAN2D_EINVAL;
   if (d->dtype != SCAN2D_F32 && d->dtype != SCAN2D_F64) return SCAN2D_EINVAL;
   if (d->reserved != 0) return SCAN2D_EINVAL;
-  if (d->state_dim > 128) return SCAN2D_EUNSUPPORTED;  // one warp spans <= 128 states (32 lanes x 4)
+  // N > 128 runs as passes over state groups of <= 128 (scan2d_groups.cu)
   return SCAN2D_OK;
 }
 
@@ -557,6 +569,7 @@ int scan2d_check_desc(const scan2d_desc* desc) { return check_desc(desc); }
 // workspace covers every plan a call with this descriptor can take.
 size_t scan2d_workspace_bytes(const scan2d_desc* desc, int op) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
+  if (desc->state_dim > kMaxKernelN) return scan2d_groups_workspace_bytes(*desc, op);
   size_t best = 0;
   bool any = false;
   for (int v = 0; v < 2; ++v) {
@@ -570,6 +583,7 @@ size_t scan2d_workspace_bytes(const scan2d_desc* desc, int op) {
 
 size_t scan2d_residual_bytes(const scan2d_desc* desc) {
   if (check_desc(desc) != SCAN2D_OK) return 0;
+  if (desc->state_dim > kMaxKernelN) return scan2d_groups_residual_bytes(*desc);
   Plan p;
   if (plan_with_flags(*desc, p, false, false) != SCAN2D_OK) return 0;
   return res_layout(*desc, p).total;
@@ -582,6 +596,12 @@ int scan2d_forward(const scan2d_desc* desc, const void* x, const void* z, const 
   const int rc = check_desc(desc);
   if (rc != SCAN2D_OK) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (desc->state_dim > kMaxKernelN) {
+    if (!x || !z || !B || !C || !A || !Dskip || !bias || !y || ((ph == nullptr) != (pv == nullptr)))
+      return SCAN2D_EINVAL;
+    return scan2d_groups_forward(*desc, x, z, B, C, A, Dskip, bias, y, ph, pv, residual, workspace,
+                                 workspace_bytes, st);
+  }
   if (desc->dtype == SCAN2D_F64)
     return forward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, y, ph, pv, residual, workspace,
                                 workspace_bytes, st);
@@ -597,6 +617,14 @@ int scan2d_backward(const scan2d_desc* desc, const void* x, const void* z, const
   const int rc = check_desc(desc);
   if (rc != SCAN2D_OK) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (desc->state_dim > kMaxKernelN) {
+    if (residual == nullptr) return SCAN2D_ESTALE;
+    if (!x || !z || !B || !C || !A || !Dskip || !bias || !dy || !dx || !dz || !dA || !dB || !dC || !dDskip ||
+        !dbias)
+      return SCAN2D_EINVAL;
+    return scan2d_groups_backward(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip,
+                                  dbias, workspace, workspace_bytes, st);
+  }
   if (desc->dtype == SCAN2D_F64)
     return backward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB,
                                  dC, dDskip, dbias, workspace, workspace_bytes, st);
@@ -610,6 +638,7 @@ int scan2d_forward_band(const scan2d_desc* desc, const void* x, const void* z, c
                         size_t workspace_bytes, scan2d_stream_t stream) {
   const int rc = check_desc(desc);
   if (rc != SCAN2D_OK) return rc;
+  if (desc->state_dim > kMaxKernelN) return SCAN2D_EUNSUPPORTED;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (desc->dtype == SCAN2D_F64)
     return forward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, y, nullptr, nullptr, residual, workspace,
@@ -625,6 +654,7 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
                          void* g_top, void* workspace, size_t workspace_bytes, scan2d_stream_t stream) {
   const int rc = check_desc(desc);
   if (rc != SCAN2D_OK) return rc;
+  if (desc->state_dim > kMaxKernelN) return SCAN2D_EUNSUPPORTED;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (desc->dtype == SCAN2D_F64)
     return backward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip,
@@ -682,6 +712,11 @@ int scan2d_bwd_f64(const scan2d_desc* desc, const double* x, const double* z, co
 int scan2d_plan_info(const scan2d_desc* desc, int op, int64_t* out8) {
   int rc = check_desc(desc);
   if (rc != SCAN2D_OK) return rc;
+  if (desc->state_dim > kMaxKernelN) {  // per state group of 128
+    scan2d_desc g = *desc;
+    g.state_dim = kMaxKernelN;
+    return scan2d_plan_info(&g, op, out8);
+  }
   if (out8 == nullptr) return SCAN2D_EINVAL;
   Plan p;
   rc = make_plan(*desc, p);

@@ -116,7 +116,7 @@ class _MetaRng:
 
 
 @pytest.mark.parametrize("H,W,N,T", [(9, 9, 2, 4), (16, 16, 16, 16), (23, 17, 3, 8), (7, 7, 2, 16),
-                                     (40, 300, 16, 16)])
+                                     (40, 300, 16, 16), (7, 9, 260, 4)])
 def test_forward_carries(orc, s2d, H, W, N, T):
     """CarryState ph / pv (engine.hpp:29-46) including edge pass-through slots."""
     b = make_batch(orc, 2, H, W, N, seed0=7, dtype="f64")

@@ -83,3 +83,33 @@ def test_wide_state_warp_kernels(orc, N, W, dtype):
     S, H = 2, 11
     b, op, y, grads = _run(orc, S, H, W, N, dtype, seed=500 + N)
     _check(orc, b, y, grads, dtype, f"warp N={N} {dtype}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,W", [(129, 12), (200, 16), (256, 40), (300, 9), (2048, 4)])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_state_groups_beyond_128(orc, N, W, dtype):
+    """N > 128 (up to the reference's 2048): passes over state groups of <= 128."""
+    S, H = 2, 7
+    b, op, y, grads = _run(orc, S, H, W, N, dtype, seed=700 + N)
+    _check(orc, b, y, grads, dtype, f"groups N={N} {dtype}")
+
+
+@pytest.mark.gpu
+def test_state_groups_shared_params():
+    """N > 128 with per-channel parameters (P < S) and shared B/C (G > 1)."""
+    from scan_cases import batch_to_torch as b2t
+
+    o = Oracle()
+    b = make_batch(o, 6, 6, 10, 150, seed0=9, dtype="f64", P=3, G=2)
+    from paper_2412_00678_b200 import tiled_scan_2d_backward, tiled_scan_2d_forward
+
+    (x, z, B, C, A, D, bias), dy = b2t(b, device="cuda")
+    res = tiled_scan_2d_forward(x, z, B, C, A, D, bias)
+    g = tiled_scan_2d_backward(res.saved, dy)
+    torch.cuda.synchronize()
+    assert rel_error(res.y.cpu().numpy(), oracle_fwd(o, b, "f64")) <= F64_Y_GATE
+    ref = oracle_bwd(o, b, "f64")
+    got = dict(dx=g.dx, dz=g.dz_raw, dA=g.da, dB=g.db, dC=g.dc, dD=g.dd, dbias=g.dbias)
+    for k, t in got.items():
+        assert rel_error(t.cpu().numpy().reshape(-1), np.asarray(ref[k]).reshape(-1)) <= F64_G_GATE, k
