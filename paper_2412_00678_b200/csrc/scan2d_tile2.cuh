@@ -286,19 +286,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// L2 prefetch of one tile's [R][CW][N] block of a B-like tensor (g offset by
-// c0 * N): exactly 32 128-byte lines for CW = 16 -- one per lane.  The loads that
-// follow a tile later then see L2 rather than HBM latency.
-template <typename TS, int N, typename T>
-__device__ __forceinline__ void prefetch_tile(const T* g, int r0, int H, size_t WN, int ncols, int lane) {
-  constexpr int LR = TS::BUR * TS::EPV * static_cast<int>(sizeof(T)) / 128;  // lines per tile row
-  if constexpr (LR >= 1 && 32 % LR == 0) {
-    const int rr = lane / LR, li = lane % LR;
-    const int row = r0 + rr;
-    if (rr < TS::R && row < H && li * 128 < ncols * N * static_cast<int>(sizeof(T)))
-      prefetch_l2(reinterpret_cast<const char*>(g + static_cast<size_t>(row) * WN) + li * 128);
-  }
-}
 
 // ------------------------------------------------------------ CTA = strips
 //
