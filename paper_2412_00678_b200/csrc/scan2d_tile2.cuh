@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
             const T av = Num<T>::exp_scaled(dj * A1[e]);
             const T gh = g4[e] + rho[e];  // engine.cpp:346
             rho[e] = av * gh;
-            const T th = gh * hl[e] * av;
+            const T th = rho[e] * hl[e];  // Gh hh(i,j-1) Abar
             dAr[e] = fma(th, dj, dAr[e]);
             dd = fma(th, A1[e], dd);
             sg = fma(gh, bc[j][e], sg);
