@@ -7,8 +7,9 @@
 // copies run concurrently on three streams ordered by events, so the PCIe
 // transfers in both directions overlap each other and the kernels.
 //
-// Device buffers, streams and events are cached per host thread and per
-// (descriptor, chunk count) and reused across calls.
+// Three device buffer sets rotate, so chunk k+2's host->device copies never
+// wait for chunk k's device->host copies to drain.  Device buffers, streams and
+// events are cached per host thread and per (descriptor, chunk count).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -39,8 +40,9 @@ struct Ctx {
   bool with_bwd = false;
   int device = -1;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[2] = {}, ev_out[2] = {}, ev_free[2] = {}, ev_start = nullptr;
-  Slot slot[2];
+  static constexpr int kSlots = 3;
+  cudaEvent_t ev_in[kSlots] = {}, ev_out[kSlots] = {}, ev_free[kSlots] = {}, ev_start = nullptr;
+  Slot slot[kSlots];
   ~Ctx() {
     for (Slot& s : slot) {
       for (void* p : s.in) cudaFree(p);
@@ -49,7 +51,7 @@ struct Ctx {
       cudaFree(s.wsf);
       cudaFree(s.wsb);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       cudaEventDestroy(ev_in[i]);
       cudaEventDestroy(ev_out[i]);
       cudaEventDestroy(ev_free[i]);
@@ -91,7 +93,7 @@ int setup(const scan2d_desc& d, int chunks, bool with_bwd) {
       cudaStreamCreateWithFlags(&c->comp, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return SCAN2D_ECUDA;
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < Ctx::kSlots; ++i)
     if (cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming) != cudaSuccess)
@@ -155,14 +157,14 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
   cudaStreamWaitEvent(c.h2d, c.ev_start, 0);
   const int nchunk = static_cast<int>((d.num_scans + c.chunk_scans - 1) / c.chunk_scans);
   for (int k = 0; k < nchunk; ++k) {
-    const int sl = k & 1;
+    const int sl = k % Ctx::kSlots;
     Slot& s = c.slot[sl];
     const int64_t s0 = static_cast<int64_t>(k) * c.chunk_scans;
     const int64_t sk = std::min<int64_t>(c.chunk_scans, d.num_scans - s0);
     size_t in[8], out[8], in0[8], out0[8];
     counts(d, sk, in, out);
     counts(d, s0, in0, out0);  // element offsets of this chunk in the host arrays
-    if (k >= 2) cudaStreamWaitEvent(c.h2d, c.ev_free[sl], 0);
+    if (k >= Ctx::kSlots) cudaStreamWaitEvent(c.h2d, c.ev_free[sl], 0);
     for (int i = 0; i < (bwd ? 8 : 7); ++i)
       if (cudaMemcpyAsync(s.in[i], static_cast<const char*>(hin[i]) + in0[i] * es, in[i] * es,
                           cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
@@ -191,7 +193,7 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
     cudaEventRecord(c.ev_free[sl], c.d2h);
   }
   // the caller's stream resumes after the last device -> host copy
-  cudaStreamWaitEvent(user, c.ev_free[(nchunk - 1) & 1], 0);
-  if (nchunk > 1) cudaStreamWaitEvent(user, c.ev_free[nchunk & 1], 0);
+  for (int k = std::max(0, nchunk - Ctx::kSlots); k < nchunk; ++k)
+    cudaStreamWaitEvent(user, c.ev_free[k % Ctx::kSlots], 0);
   return cudaGetLastError() == cudaSuccess ? SCAN2D_OK : SCAN2D_ECUDA;
 }
