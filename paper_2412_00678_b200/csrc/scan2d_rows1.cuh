@@ -180,6 +180,21 @@ struct Rows1Job {
   T x[J], z[J], b[J], c[J], dy[J];
 };
 
+// one lane's J elements, global -> shared, zero-filled when !ok (cp.async .ca
+// takes 4 / 8 / 16 bytes: the lane's own columns, no cross-lane traffic)
+template <typename T, int J>
+__device__ __forceinline__ void cp_lane(uint32_t sdst, const T* g, bool ok) {
+  constexpr int BYTES = J * static_cast<int>(sizeof(T));
+  constexpr int PIECE = BYTES < 16 ? BYTES : 16;
+  static_assert(PIECE == 4 || PIECE == 8 || PIECE == 16, "cp.async size");
+  const int src = ok ? PIECE : 0;
+#pragma unroll
+  for (int o = 0; o < BYTES; o += PIECE)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sdst + o),
+                 "l"(reinterpret_cast<const char*>(g) + o), "n"(PIECE), "r"(src)
+                 : "memory");
+}
+
 template <typename T, int J>
 __device__ __forceinline__ void load_job(Rows1Job<T, J>& jb, const T* xg, const T* zg, const T* Bg, const T* Cg,
                                          const T* yg, int row, int H, int W, bool ok, bool rev) {
@@ -225,21 +240,44 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
   if (a.gbot != nullptr && ok) ldg_states<T, J>(dn, a.gbot + s * W + q * J);
   T dA_acc = T(0), db_acc = T(0), dD_acc = T(0);
 
-  // job order per band: F rows r0 .. r0+K-1, then R rows r0+K-1 .. r0.  Loads run
-  // NB - 1 jobs ahead in NB register buffers (2K jobs per band, so the buffer of
-  // a job is static): NB = 2 at J = 4 (register budget), 4 below.
-  constexpr int NB = J >= 4 ? 2 : 4;
-  static_assert((2 * K) % NB == 0, "job buffers must tile a band");
-  Rows1Job<T, J> jb[NB];
+  // job order per band: F rows r0 .. r0+K-1, then R rows r0+K-1 .. r0.  Each
+  // lane streams its own columns of the next NJ-1 row-jobs into a private
+  // shared-memory ring with cp.async (no registers held for the prefetch).
+  constexpr int NJ = J * sizeof(T) > 16 ? 2 : 4;  // static smem <= 48 KB (fp64 J = 4 never runs)
+  static_assert((2 * K) % NJ == 0, "job slots must tile a band");
+  __shared__ __align__(16) T ring[4][NJ][5][32][J];  // [warp in CTA][slot][operand][lane][J]
+  T(*my)[5][32][J] = ring[(threadIdx.x >> 5) & 3];
+  const int lane = threadIdx.x & 31;
   // job jj counted from band bb's first job (jj >= 2K: the band above)
   auto issue = [&](int bb, int jj) {
     const int band = bb - jj / (2 * K), loc = jj % (2 * K);
     const bool rev = loc >= K;
     const int row = band * K + (rev ? 2 * K - 1 - loc : loc);
-    load_job<T, J>(jb[jj % NB], xg, zg, Bg, Cg, yg, row, H, W, ok && band >= 0, rev);
+    const bool rv = ok && band >= 0 && row >= 0 && row < H;
+    const size_t o = static_cast<size_t>(rv ? row : 0) * W;
+    T(*sl)[32][J] = my[jj % NJ];
+    cp_lane<T, J>(smem_u32(sl[0][lane]), xg + o, rv);
+    cp_lane<T, J>(smem_u32(sl[1][lane]), zg + o, rv);
+    cp_lane<T, J>(smem_u32(sl[2][lane]), Bg + o, rv);
+    if (rev) {
+      cp_lane<T, J>(smem_u32(sl[3][lane]), Cg + o, rv);
+      cp_lane<T, J>(smem_u32(sl[4][lane]), yg + o, rv);
+    }
+    cp_async_commit();
+  };
+  auto fetch = [&](int jj, Rows1Job<T, J>& jb, bool rev) {
+    cp_async_wait<NJ - 1>();
+    T(*sl)[32][J] = my[jj % NJ];
+    lds_vec<T, J>(jb.x, sl[0][lane]);
+    lds_vec<T, J>(jb.z, sl[1][lane]);
+    lds_vec<T, J>(jb.b, sl[2][lane]);
+    if (rev) {
+      lds_vec<T, J>(jb.c, sl[3][lane]);
+      lds_vec<T, J>(jb.dy, sl[4][lane]);
+    }
   };
 #pragma unroll
-  for (int jj = 0; jj < NB - 1; ++jj) issue(nb - 1, jj);
+  for (int jj = 0; jj < NJ - 1; ++jj) issue(nb - 1, jj);
   for (int b = nb - 1; b >= 0; --b) {
     const int r0 = b * K;
     T hp0[J];  // h of the row above the band (checkpoint / band carry / zeros)
@@ -259,8 +297,9 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
       for (int k = 0; k < J; ++k) hcur[k] = hp0[k];
 #pragma unroll
       for (int r = 0; r < K; ++r) {
-        issue(b, r + NB - 1);
-        Rows1Job<T, J>& cur = jb[r % NB];
+        issue(b, r + NJ - 1);
+        Rows1Job<T, J> cur;
+        fetch(r, cur, false);
         T av[J], u[J];
         T hl = T(0), ap = T(1);
 #pragma unroll
@@ -287,8 +326,9 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
 #pragma unroll
     for (int rr = K - 1; rr >= 0; --rr) {
       const int jidx = K + (K - 1 - rr);  // job index within the band: K .. 2K-1
-      issue(b, jidx + NB - 1);
-      Rows1Job<T, J>& cur = jb[jidx % NB];
+      issue(b, jidx + NJ - 1);
+      Rows1Job<T, J> cur;
+      fetch(jidx, cur, true);
       const int i = r0 + rr;
       T d[J], av[J], sg[J], G[J];
       T rl = T(0), ap = T(1);  // lane aggregate of the reverse horizontal map
