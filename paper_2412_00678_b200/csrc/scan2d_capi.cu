@@ -343,7 +343,7 @@ int plan_with_flags(const scan2d_desc& d, Plan& p, bool xvec, bool bvec, bool em
 size_t slot_size(int dtype) { return dtype == SCAN2D_F64 ? 16 : 8; }
 
 struct WsLayout {
-  size_t ticket = 0, hcarry = 0, rcarry = 0, part = 0, dbc = 0, total = 0;
+  size_t ticket = 0, cnt = 0, hcarry = 0, rcarry = 0, part = 0, dbc = 0, total = 0;
 };
 
 // forward workspace: [ticket][hcarry (when no residual is given)]
@@ -355,6 +355,10 @@ WsLayout ws_layout(const scan2d_desc& d, const Plan& p, int op) {
   size_t off = 0;
   L.ticket = off;
   off += kAlign;
+  if (op == SCAN2D_OP_BWD) {  // per-scan finish counters, right after the ticket (one memset)
+    L.cnt = off;
+    off += align_up(sizeof(int) * S);
+  }
   if (op == SCAN2D_OP_FWD) {
     L.hcarry = off;
     off += align_up(ss * S * p.nq * d.height * d.state_dim);
@@ -536,16 +540,28 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   a.part = reinterpret_cast<T*>(w + L.part);
   a.rcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.rcarry);
   a.ticket = reinterpret_cast<int*>(w + L.ticket);
-  if (p.b.wreal > 1 && cudaMemsetAsync(a.ticket, 0, sizeof(int), stream) != cudaSuccess)
+  // per-scan parameters: the kernels finish dA / dbias / dD themselves (fixed
+  // strip order, no extra launch); shared parameters need the reduction kernel
+  const bool fuse = (p.b.tile || p.b.rows1) && d.params_period == d.num_scans;
+  a.fuse = fuse;
+  a.scan_cnt = reinterpret_cast<int*>(w + L.cnt);
+  a.dA_out = static_cast<T*>(dA);
+  a.dbias_out = static_cast<T*>(dbias);
+  a.dD_out = static_cast<T*>(dDskip);
+  if (p.b.wreal > 1 &&
+      cudaMemsetAsync(a.ticket, 0, L.cnt + sizeof(int) * static_cast<size_t>(d.num_scans) - L.ticket, stream) !=
+          cudaSuccess)
     return SCAN2D_ECUDA;
   int launches = 0;
   if (s2d::launch_bwd<T>(a, stream) != cudaSuccess) return SCAN2D_ECUDA;
   ++launches;
-  if (s2d::launch_reduce_params<T>(a.part, d.num_scans, p.b.wreal, d.params_period, d.state_dim,
-                                   static_cast<T*>(dA), static_cast<T*>(dbias),
-                                   static_cast<T*>(dDskip), stream) != cudaSuccess)
-    return SCAN2D_ECUDA;
-  ++launches;
+  if (!fuse) {
+    if (s2d::launch_reduce_params<T>(a.part, d.num_scans, p.b.wreal, d.params_period, d.state_dim,
+                                     static_cast<T*>(dA), static_cast<T*>(dbias),
+                                     static_cast<T*>(dDskip), stream) != cudaSuccess)
+      return SCAN2D_ECUDA;
+    ++launches;
+  }
   if (d.bc_group > 1) {
     const int64_t groups = d.num_scans / d.bc_group;
     if (s2d::launch_reduce_group<T>(dB_ps, groups, d.bc_group, hwn, static_cast<T*>(dB), stream) !=

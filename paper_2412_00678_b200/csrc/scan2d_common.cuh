@@ -467,6 +467,13 @@ struct Args {
   T* dB;       // [S][H][W][N] (per scan; reduced over the B/C group afterwards when G > 1)
   T* dC;
   T* part;     // per (scan, warp) partials: [S][wreal_b][N + 2] = dA[N], dbias, dD
+  // fused parameter-gradient reduction (per-scan parameters, P == S): the last
+  // strip of a scan to finish sums the scan's partials in strip order
+  int fuse;
+  int* scan_cnt;  // [S] strips finished per scan (zeroed before the launch)
+  T* dA_out;
+  T* dbias_out;
+  T* dD_out;
   CarrySlot<T>* rcarry;  // reverse carry at backward warp boundaries, [S][wreal_b-1][H][N]
   int* ticket;           // warp ticket counter (zeroed before each chained launch)
   uint32_t epoch;        // tag base of this launch (see row_tag)

@@ -394,10 +394,16 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
     dD_acc += __shfl_xor_sync(kFull, dD_acc, o, SEG);
   }
   if (q == 0 && id.s < a.S) {
-    T* part = a.part + static_cast<size_t>(id.s) * 3;  // [S][1][N + 2], N = 1
-    part[0] = dA_acc;
-    part[1] = db_acc;
-    part[2] = dD_acc;
+    if (a.fuse) {  // P == S: one warp segment owns the scan -- write the gradients directly
+      a.dA_out[id.s] = dA_acc;
+      a.dbias_out[id.s] = db_acc;
+      a.dD_out[id.s] = dD_acc;
+    } else {
+      T* part = a.part + static_cast<size_t>(id.s) * 3;  // [S][1][N + 2], N = 1
+      part[0] = dA_acc;
+      part[1] = db_acc;
+      part[2] = dD_acc;
+    }
   }
 }
 

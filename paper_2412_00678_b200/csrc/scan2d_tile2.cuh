@@ -958,6 +958,30 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     part[N] = dbias_acc;
     part[N + 1] = dD_acc;
   }
+  if (a.fuse) {  // P == S: the scan's last strip adds the partials, strip order fixed
+    bool last = ge.wreal == 1;
+    if (!last) {
+      __threadfence();
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) old = atomicAdd(a.scan_cnt + s, 1);
+      last = __shfl_sync(kFull, old, 0) == ge.wreal - 1;
+      if (last) __threadfence();
+    }
+    if (last) {
+      const T* ps = a.part + static_cast<size_t>(s) * ge.wreal * (N + 2);
+      for (int k = lane; k < N + 2; k += 32) {
+        T acc = T(0);
+        for (int w = 0; w < ge.wreal; ++w) acc += __ldcg(ps + static_cast<size_t>(w) * (N + 2) + k);
+        if (k < N)
+          a.dA_out[static_cast<size_t>(s) * N + k] = acc;
+        else if (k == N)
+          a.dbias_out[s] = acc;
+        else
+          a.dD_out[s] = acc;
+      }
+    }
+  }
 }
 
 }  // namespace s2d
