@@ -160,6 +160,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
   p.b = make_geo(d, true);
   p.f = make_geo(d, false);
+  p.pfd = env_int("SCAN2D_ROWS1_PFD", 8);
   if (rows1_shape(d)) {
     p.K = 4;
     p.nb = static_cast<int>(ceil_div(d.height, p.K));

@@ -437,6 +437,7 @@ struct Plan {
   int Q;      // column interval of the saved horizontal carries (= b.colsw)
   int nq;     // ceil(W / Q) - 1 carry boundaries per row
   int warp_ok;  // the warp kernels' geometry fits this residual layout (else tile / rows1 kernels only)
+  int pfd;      // N = 1 forward: L2 prefetch distance in rows
 };
 
 template <typename T>

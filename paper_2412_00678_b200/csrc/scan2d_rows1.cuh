@@ -154,8 +154,8 @@ __global__ void __launch_bounds__(128) scan2d_fwd_rows1_kernel(const Args<T> a) 
           if (a.vbot != nullptr && i == H - 1) stg_row<T, J>(a.vbot + s * W + q * J, h);
         }
         // L2 prefetch of row i + 2K, then refill this slot with row i + K
-        if (ok && i + 2 * K < H) {
-          const size_t o2 = static_cast<size_t>(i + 2 * K) * W;
+        if (ok && i + a.plan.pfd < H) {
+          const size_t o2 = static_cast<size_t>(i + a.plan.pfd) * W;
           prefetch_l2(xg + o2);
           prefetch_l2(zg + o2);
           prefetch_l2(Bg + o2);
