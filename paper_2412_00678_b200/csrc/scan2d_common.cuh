@@ -83,8 +83,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
                : "memory");
 }
+// No "memory" clobber: the destination slot is fenced by the __syncwarp that
+// ends its previous use and by cp_async_wait (which has one) before its next
+// read, so the compiler may schedule the issue among surrounding work.
 __device__ __forceinline__ void cp_async16_raw(uint32_t smem_addr, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_elem(float* smem, const float* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem)
