@@ -9,32 +9,34 @@
 //   dAbar = Gh hh(i,j-1) + G h(i-1,j);  dA += dAbar delta Abar;  ddelta = sum_d dAbar Abar A + Gh B x
 //   dB = Gh delta x;  dC = dy h;  dx = D dy + delta sum_d Gh B;  dz = ddelta sigmoid(z+bias)
 //
-// Decomposition (one warp = one CTA = one 16-column STRIP of one scan, walking
-// the strip in tiles of R rows; R * N / SH = 32):
+// Decomposition (one warp = one 16-column STRIP of one scan, walking the strip
+// in tiles of R rows; R * N / SH = 32):
 //  * row lanes (r, q) own row r of the tile and SH consecutive states: they run
 //    the horizontal recurrences (hh forward, Gh backward) with the carry in
 //    registers.  Their B operands come straight from HBM into registers
-//    (8/16-byte loads, 64 contiguous bytes per row) one tile AHEAD -- B never
-//    touches shared memory;
+//    (8/16-byte loads, 64 contiguous bytes per row), the next tile's loaded
+//    column by column as each column is retired -- B never touches shared
+//    memory;
 //  * column lanes (j, s) own column j and SV = N/2 states: they run the
 //    vertical recurrences (h forward, G backward) with the state in registers
 //    across tiles.  Their C operands stream through shared memory with
-//    cp.async, also one tile ahead;
+//    cp.async, one tile ahead;
 //  * the only transposes are hh (row -> column lanes) and G (column -> row
 //    lanes), through three rotating [R][16 N + N] slots (C of this tile, hh of
-//    this tile, C of the next tile); the padding keeps both access patterns
-//    bank-conflict free.
+//    this tile, C of the next tile); the row padding and a per-column rotation
+//    of the column lanes' 16-byte units keep both access patterns
+//    bank-conflict free;
 //  * the backward splits dAbar = Gh hh(i,j-1) + G h(i-1,j): the column lanes
 //    fold the G h(i-1,j) half into dA and ddelta themselves (they own h), so
-//    h never has to be transposed back to the row lanes.
-//  * strips exchange the horizontal carries through global memory as tagged
-//    8-byte words (scan2d_common.cuh); tickets order the strips so every
-//    producer is resident before its consumer.  The forward publishes hh at
-//    every strip boundary (kept as the training residual) and h at the last row
-//    of every tile (checkpoints), so the backward recomputes instead of storing
-//    states.
-// Shared memory per warp (fp32, N = 16): 15.4 KB -> 13 warps per SM, so the
-// 1664 strips of a 128 x 200 x 200 batch are resident in one wave.
+//    h never has to be transposed back to the row lanes;
+//  * a CTA holds up to 13 (forward) / 12 (backward) warps = consecutive strips
+//    in scan-major order; neighbouring strips of one scan in one CTA pass the
+//    horizontal carry through an mbarrier-guarded shared-memory ring, strips in
+//    different CTAs through tagged 8-byte words in global memory (CTA tickets
+//    keep producers resident).  The forward publishes hh at every strip
+//    boundary (kept as the training residual) and h at the last row of every
+//    tile (checkpoints), so the backward recomputes instead of storing states.
+// Shared memory per warp (fp32, N = 16): 14.3 KB forward, 16.5 KB backward.
 #pragma once
 
 #include "scan2d_fwd.cuh"
