@@ -1,6 +1,7 @@
 """Time forward (training, residual saved) and backward for arbitrary shapes.
 
-usage: python tools/time_shapes.py S,H,W,N [S,H,W,N ...]   (fp32, CUDA events, inputs resident)
+usage: python tools/time_shapes.py S,H,W,N[,G] ...   (fp32, CUDA events, inputs resident;
+G = scans sharing one B/C block, the model.cpp layout)
 Prints ms and algorithmic GB/s (memsim.cpp:45-46 counting) per direction.
 """
 import json
@@ -13,14 +14,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2412_00678_b200.api import Scan2dOp  # noqa: E402
 
 
-def run(S, H, W, N, reps=10):
+def run(S, H, W, N, G=1, reps=10):
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(1)
     r = lambda *s: torch.randn(*s, generator=g, device=dev)
-    x, z, B, C, dy = r(S, H, W), r(S, H, W), r(S, H, W, N), r(S, H, W, N), r(S, H, W)
+    x, z, B, C, dy = r(S, H, W), r(S, H, W), r(S // G, H, W, N), r(S // G, H, W, N), r(S, H, W)
     A = -(0.05 + 0.9 * torch.rand(S, N, generator=g, device=dev))
     D, bias = r(S), torch.rand(S, generator=g, device=dev) - 0.5
-    op = Scan2dOp(S, H, W, N, tile=16, device=dev, with_backward=True)
+    op = Scan2dOp(S, H, W, N, tile=16, bc_group=G, device=dev, with_backward=True)
     ins = (x, z, B, C, A, D, bias)
     for _ in range(3):
         op.forward(*ins, save=True)
@@ -38,9 +39,11 @@ def run(S, H, W, N, reps=10):
         tf += ev[0].elapsed_time(ev[1])
         tb += ev[1].elapsed_time(ev[2])
     tf, tb = tf / reps, tb / reps
-    hw = S * H * W * 4
-    fb, bb = hw * (3 + 2 * N), hw * (5 + 4 * N)
-    return {"shape": [S, H, W, N], "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4),
+    # per-scan B/C (G = 1): memsim.cpp:45-46; shared B/C: B/C bytes once per group
+    cells = H * W * 4
+    fb = cells * (3 * S + 2 * N * (S // G))
+    bb = cells * (5 * S + 4 * N * (S // G))
+    return {"shape": [S, H, W, N, G], "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4),
             "fwd_gbs": round(fb / tf / 1e6, 1), "bwd_gbs": round(bb / tb / 1e6, 1), "plan_f": op.plan()}
 
 
