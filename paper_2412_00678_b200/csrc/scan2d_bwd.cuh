@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   const bool has_pred = lm.wpos > 0;
   const bool has_succ = lm.wpos + 1 < ge.wreal;
   // saved forward carry into this warp's first column (residual, no waiting)
-  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((sc * nq + (lm.c0 / Q - 1)) * H) * N + q * SPL : nullptr;
+  const T* hc_in = has_pred ? a.hres + ((sc * nq + (lm.c0 / Q - 1)) * H) * N + q * SPL : nullptr;
   // reverse chain: receive from wpos+1, send to wpos-1 ([S][wreal-1][H][N])
   const int wb = ge.wreal - 1;
   const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((sc * wb + lm.wpos) * H) * N + q * SPL : nullptr;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
       }
       T ew[SPL];
       if (has_pred)
-        carry_get<T, SPL>(hc_in + static_cast<size_t>(i) * N, ew, nvalid);
+        load_states<T, SPL>(ew, hc_in + static_cast<size_t>(i) * N, nvalid);
       else {
 #pragma unroll
         for (int e = 0; e < SPL; ++e) ew[e] = T(0);

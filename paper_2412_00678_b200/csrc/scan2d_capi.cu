@@ -347,7 +347,7 @@ struct WsLayout {
   size_t ticket = 0, cnt = 0, hcarry = 0, rcarry = 0, part = 0, dbc = 0, total = 0;
 };
 
-// forward workspace: [ticket][hcarry (when no residual is given)]
+// forward workspace: [ticket][hcarry (the forward's tagged carry chain)]
 // backward workspace: [ticket][rcarry][part][per-scan dB, dC (G > 1)]
 WsLayout ws_layout(const scan2d_desc& d, const Plan& p, int op) {
   const size_t es = dtype_size(d.dtype), ss = slot_size(d.dtype);
@@ -378,17 +378,17 @@ WsLayout ws_layout(const scan2d_desc& d, const Plan& p, int op) {
 }
 
 struct ResLayout {
-  size_t ckpt = 0, hcarry = 0, total = 0;
+  size_t ckpt = 0, hres = 0, total = 0;
 };
 
 ResLayout res_layout(const scan2d_desc& d, const Plan& p) {
-  const size_t es = dtype_size(d.dtype), ss = slot_size(d.dtype);
+  const size_t es = dtype_size(d.dtype);
   const size_t S = static_cast<size_t>(d.num_scans);
   ResLayout R;
   R.ckpt = 0;
   size_t off = align_up(es * S * (p.nb - 1) * d.width * d.state_dim);
-  R.hcarry = off;
-  off += align_up(ss * S * p.nq * d.height * d.state_dim);
+  R.hres = off;
+  off += align_up(es * S * p.nq * d.height * d.state_dim);
   R.total = std::max<size_t>(off, kAlign);
   return R;
 }
@@ -474,11 +474,12 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
     const ResLayout R = res_layout(d, p);
     unsigned char* r = static_cast<unsigned char*>(residual);
     a.ckpt = reinterpret_cast<T*>(r + R.ckpt);
-    a.hcarry = reinterpret_cast<s2d::CarrySlot<T>*>(r + R.hcarry);
+    a.hres = reinterpret_cast<T*>(r + R.hres);
   } else {
     a.ckpt = nullptr;
-    a.hcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.hcarry);
+    a.hres = nullptr;
   }
+  a.hcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.hcarry);
   if (p.f.wreal > 1 && cudaMemsetAsync(a.ticket, 0, sizeof(int), stream) != cudaSuccess)
     return SCAN2D_ECUDA;
   if (ph != nullptr) {
@@ -522,7 +523,8 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   set_flags(a, xvec, bvec, yvec);
   a.dy = static_cast<const T*>(dy);
   a.ckpt = const_cast<T*>(reinterpret_cast<const T*>(r + R.ckpt));
-  a.hcarry = const_cast<s2d::CarrySlot<T>*>(reinterpret_cast<const s2d::CarrySlot<T>*>(r + R.hcarry));
+  a.hres = const_cast<T*>(reinterpret_cast<const T*>(r + R.hres));
+  a.hcarry = nullptr;
   if ((vtop != nullptr || gbot != nullptr || gtop != nullptr) && !p.b.tile) return SCAN2D_EUNSUPPORTED;
   a.vtop = static_cast<const T*>(vtop);
   a.gbot = static_cast<const T*>(gbot);

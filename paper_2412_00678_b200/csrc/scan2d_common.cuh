@@ -283,6 +283,19 @@ __device__ __forceinline__ void carry_get(const CarrySlot<T>* p, T (&v)[SPL], in
   for (int e = 0; e < SPL; ++e) v[e] = e < nvalid ? CarrySlot<T>::get(p + e) : T(0);
 }
 
+// plain (untagged) residual copies of carries: the first nvalid states
+template <typename T, int SPL>
+__device__ __forceinline__ void store_states(T* p, const T (&v)[SPL], int nvalid) {
+#pragma unroll
+  for (int e = 0; e < SPL; ++e)
+    if (e < nvalid) p[e] = v[e];
+}
+template <typename T, int SPL>
+__device__ __forceinline__ void load_states(T (&v)[SPL], const T* p, int nvalid) {
+#pragma unroll
+  for (int e = 0; e < SPL; ++e) v[e] = e < nvalid ? p[e] : T(0);
+}
+
 // ------------------------------------------------------- warp collectives
 
 // Reduce-scatter of v[J] over the LPC lanes of a chunk (lane bits below LPC).
@@ -464,7 +477,8 @@ struct Args {
   T* vbot;              // forward: h of the band's last row, [S][W][N] (NULL = not wanted)
   const T* gbot;        // backward: Abar G of the row below the band, [S][W][N] (NULL = zeros)
   T* gtop;              // backward: Abar G of the band's first row, [S][W][N] (NULL = not wanted)
-  CarrySlot<T>* hcarry; // horizontal carry at every Q-column boundary, [S][nq][H][N]
+  CarrySlot<T>* hcarry; // forward chain: tagged horizontal carries at Q-column boundaries, [S][nq][H][N]
+  T* hres;              // residual: plain horizontal carries at every Q-column boundary, [S][nq][H][N]
   // backward outputs
   T* dx;
   T* dz;

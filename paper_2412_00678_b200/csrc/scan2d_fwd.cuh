@@ -148,9 +148,11 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
   CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((sc * nq + (lm.c0 / Q - 1)) * H) * N + q * SPL : nullptr;
   CarrySlot<T>* hc_out =
       has_succ ? a.hcarry + ((sc * nq + ((lm.c0 + ge.colsw) / Q - 1)) * H) * N + q * SPL : nullptr;
-  // chunk starting on an interior Q boundary: its carry-in is saved for the backward
+  // residual (plain values): the warp's outgoing carry, and the carry-in of a
+  // chunk starting on an interior Q boundary
+  T* hr_out = save && has_succ ? a.hres + ((sc * nq + ((lm.c0 + ge.colsw) / Q - 1)) * H) * N + q * SPL : nullptr;
   const bool chunk_q = save && cis > 0 && (lm.colc % Q) == 0 && lm.colc < W;
-  CarrySlot<T>* hc_mid = chunk_q ? a.hcarry + ((sc * nq + (lm.colc / Q - 1)) * H) * N + q * SPL : nullptr;
+  T* hr_mid = chunk_q ? a.hres + ((sc * nq + (lm.colc / Q - 1)) * H) * N + q * SPL : nullptr;
   T* yrow = a.y + sc * HW;
 
   T hv[J][SPL];
@@ -265,11 +267,14 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
           const T Lt = __shfl_sync(kFull, Lc[e], (CPW - 1) * LPC + q);
           out[e] = fma(Pt, ew[e], Lt);
         }
-        if (lm.c == CPW - 1) carry_put<T, SPL>(hc_out + static_cast<size_t>(i) * N, out, tag, nvalid);
+        if (lm.c == CPW - 1) {
+          carry_put<T, SPL>(hc_out + static_cast<size_t>(i) * N, out, tag, nvalid);
+          if (save) store_states<T, SPL>(hr_out + static_cast<size_t>(i) * N, out, nvalid);
+        }
       }
 #pragma unroll
       for (int e = 0; e < SPL; ++e) hh[e] = fma(Pe[e], ew[e], Le[e]);
-      if (chunk_q) carry_put<T, SPL>(hc_mid + static_cast<size_t>(i) * N, hh, tag, nvalid);
+      if (chunk_q) store_states<T, SPL>(hr_mid + static_cast<size_t>(i) * N, hh, nvalid);
     }
 
     // ---- horizontal then vertical recurrence, C readout

@@ -449,7 +449,9 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   const bool pred_ring = has_pred && id.wi > 0;
   const bool succ_ring = has_succ && id.wi + 1 < id.nw;
   const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (wpos - 1)) * H) * N + q1 * SH : nullptr;
-  CarrySlot<T>* hc_out = has_succ ? a.hcarry + ((s * nq + wpos) * H) * N + q1 * SH : nullptr;
+  CarrySlot<T>* hc_out = has_succ && !succ_ring ? a.hcarry + ((s * nq + wpos) * H) * N + q1 * SH : nullptr;
+  // residual copy of every boundary carry (plain values, read by the backward)
+  T* hr_out = save && has_succ ? a.hres + ((s * nq + wpos) * H) * N + q1 * SH : nullptr;
   const int jg2 = c0 + j2;
   const bool col_ok = j2 < ncols;
 
@@ -545,8 +547,9 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
       }
       // strips other than the last are full (ncols == CW): hh is the boundary carry
       if (succ_ring) ring.put(id.wi, t, lane, hh);
-      if (has_succ && row_ok && (save || !succ_ring))
+      if (has_succ && row_ok && !succ_ring)
         carry_put<T, SH>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
+      if (save && has_succ && row_ok) stg_stream<T, SH>(hr_out + static_cast<size_t>(i1) * N, hh);
     }
     __syncwarp();
 
@@ -654,7 +657,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const bool succ_ring = has_succ && id.wi > 0;
   const bool pred_ring = has_pred && id.wi + 1 < id.nw;
   // saved forward carries sit on the forward's 16-column grid (plan.Q)
-  const CarrySlot<T>* hc_in = has_pred ? a.hcarry + ((s * nq + (c0 / a.plan.Q - 1)) * H) * N + q1 * SH : nullptr;
+  const T* hc_in = has_pred ? a.hres + ((s * nq + (c0 / a.plan.Q - 1)) * H) * N + q1 * SH : nullptr;
   const int wb = ge.wreal - 1;
   const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
   CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   for (int e = 0; e < SH; ++e) hh0n[e] = T(0);
   {
     const int ib = (ntiles - 1) * R + r1;
-    if (has_pred && ib < H) carry_get<T, SH>(hc_in + static_cast<size_t>(ib) * N, hh0n, SH);
+    if (has_pred && ib < H) ldg_states<T, SH>(hh0n, hc_in + static_cast<size_t>(ib) * N);
   }
 
   for (int t = ntiles - 1; t >= 0; --t) {
@@ -718,7 +721,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     T hh0[SH];
 #pragma unroll
     for (int e = 0; e < SH; ++e) hh0[e] = hh0n[e], hh0n[e] = T(0);
-    if (has_pred && t > 0) carry_get<T, SH>(hc_in + static_cast<size_t>(i1 - R) * N, hh0n, SH);
+    if (has_pred && t > 0) ldg_states<T, SH>(hh0n, hc_in + static_cast<size_t>(i1 - R) * N);
     CarryPre<T, SH> rpre;
     if constexpr (sizeof(T) == 4) {
       if (has_succ && !succ_ring && row_ok)
