@@ -137,7 +137,8 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
  * memory, engine.hpp:88-102) ----
  * One training step -- forward, and backward when dy != NULL -- on HOST
  * pointers with the layouts above.  The S scans are processed in `chunks`
- * groups through two device buffer sets: host->device copies of chunk k, the
+ * groups (the first and last split further into 1/8, 1/8, 1/4, 1/2 pieces)
+ * through three device buffer sets: host->device copies of chunk k, the
  * kernels of chunk k-1 and device->host copies of chunk k-2 overlap on three
  * internal streams; `stream` is joined at both ends (call
  * cudaStreamSynchronize(stream) before reading the outputs).  Host buffers

@@ -1,14 +1,19 @@
 // scan2d_host.cu -- host-operand entry point (include/scan2d_cuda.h,
 // scan2d_train_host): the reference API takes and returns host data
 // (engine.hpp:88-102, Grid<T> holds std::vector), so the drop-in path is
-// host -> device -> scan -> host.  This runtime pipelines it: the S scans go in
-// `chunks` groups through two device buffer sets; chunk k's host->device
-// copies, chunk k-1's forward + backward kernels and chunk k-2's device->host
-// copies run concurrently on three streams ordered by events, so the PCIe
-// transfers in both directions overlap each other and the kernels.
+// host -> device -> scan -> host.  This runtime pipelines it: the S scans go
+// through the device in chunks; chunk k's host->device copies, chunk k-1's
+// forward + backward kernels and chunk k-2's device->host copies run
+// concurrently on three streams ordered by events, so the PCIe transfers in
+// both directions overlap each other and the kernels.
 //
 // Three device buffer sets rotate, so chunk k+2's host->device copies never
-// wait for chunk k's device->host copies to drain.  Device buffers, streams and
+// wait for chunk k's device->host copies to drain.  The per-scan parameters
+// (A, Dskip, bias) go over once before the first chunk and their gradients come
+// back once after the last, so a chunk costs five copies each way.  The first
+// and the last base chunk are split into 1/8, 1/8, 1/4, 1/2 pieces (ramp): the
+// device->host direction starts, and the host->device direction finishes, after
+// one small piece instead of one whole chunk.  Device buffers, streams and
 // events are cached per host thread and per (descriptor, chunk count).
 #include <cuda_runtime.h>
 
@@ -16,6 +21,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "../../include/scan2d_cuda.h"
@@ -24,10 +30,12 @@ namespace {
 
 size_t es_of(int dtype) { return dtype == SCAN2D_F64 ? 8 : 4; }
 
+// per-chunk operands: inputs x z B C dy | outputs y dx dz dB dC
+constexpr int kIn = 5, kOut = 5;
+
 struct Slot {
-  // inputs: x z B C A D bias dy | outputs: y dx dz dA dB dC dD dbias
-  void* in[8] = {};
-  void* out[8] = {};
+  void* in[kIn] = {};
+  void* out[kOut] = {};
   void* residual = nullptr;
   void* wsf = nullptr;
   void* wsb = nullptr;
@@ -37,6 +45,9 @@ struct Slot {
 struct Ctx {
   scan2d_desc desc{};
   int chunks = 0, chunk_scans = 0;
+  std::vector<std::pair<int64_t, int64_t>> sched;  // (first scan, scans) per chunk
+  void* par[3] = {};   // A [S][N], Dskip [S], bias [S] (whole problem)
+  void* dpar[3] = {};  // dA, dDskip, dbias
   bool with_bwd = false;
   int device = -1;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
@@ -44,6 +55,8 @@ struct Ctx {
   cudaEvent_t ev_in[kSlots] = {}, ev_out[kSlots] = {}, ev_free[kSlots] = {}, ev_start = nullptr;
   Slot slot[kSlots];
   ~Ctx() {
+    for (void* p : par) cudaFree(p);
+    for (void* p : dpar) cudaFree(p);
     for (Slot& s : slot) {
       for (void* p : s.in) cudaFree(p);
       for (void* p : s.out) cudaFree(p);
@@ -67,13 +80,48 @@ thread_local std::unique_ptr<Ctx> g_ctx;
 
 bool same(const scan2d_desc& a, const scan2d_desc& b) { return std::memcmp(&a, &b, sizeof(a)) == 0; }
 
-// per-scan element counts of the eight inputs / outputs (P == S, G == 1 per chunk)
-void counts(const scan2d_desc& d, int64_t s, size_t (&in)[8], size_t (&out)[8]) {
+// element counts of the per-chunk operands for s scans (P == S, G == 1)
+void counts(const scan2d_desc& d, int64_t s, size_t (&in)[kIn], size_t (&out)[kOut]) {
   const size_t hw = static_cast<size_t>(d.height) * d.width, n = d.state_dim;
   const size_t S = static_cast<size_t>(s);
-  const size_t c[8] = {S * hw, S * hw, S * hw * n, S * hw * n, S * n, S, S, S * hw};
-  const size_t o[8] = {S * hw, S * hw, S * hw, S * n, S * hw * n, S * hw * n, S, S};
-  for (int i = 0; i < 8; ++i) in[i] = c[i], out[i] = o[i];
+  const size_t c[kIn] = {S * hw, S * hw, S * hw * n, S * hw * n, S * hw};
+  const size_t o[kOut] = {S * hw, S * hw, S * hw, S * hw * n, S * hw * n};
+  for (int i = 0; i < kIn; ++i) in[i] = c[i];
+  for (int i = 0; i < kOut; ++i) out[i] = o[i];
+}
+
+// chunk schedule: `chunks` base chunks of c0 scans; the first and the last are
+// split into 1/8, 1/8, 1/4, 1/2 (resp. reversed) pieces when large enough
+std::vector<std::pair<int64_t, int64_t>> schedule(int64_t S, int chunks, int64_t c0) {
+  std::vector<int64_t> sizes;
+  auto ramp = [&](int64_t n, bool up) {
+    std::vector<int64_t> p;
+    if (n >= 8)
+      p = {n / 8, n / 8, n / 4, n - n / 8 - n / 8 - n / 4};
+    else
+      p = {n};
+    if (!up) std::reverse(p.begin(), p.end());
+    for (int64_t v : p) sizes.push_back(v);
+  };
+  int64_t left = S;
+  for (int k = 0; k < chunks && left > 0; ++k) {
+    const int64_t n = std::min(c0, left);
+    left -= n;
+    if (chunks > 1 && k == 0)
+      ramp(n, true);
+    else if (chunks > 1 && left == 0)
+      ramp(n, false);
+    else
+      sizes.push_back(n);
+  }
+  std::vector<std::pair<int64_t, int64_t>> out;
+  int64_t s0 = 0;
+  for (int64_t v : sizes) {
+    if (v <= 0) continue;
+    out.emplace_back(s0, v);
+    s0 += v;
+  }
+  return out;
 }
 
 int setup(const scan2d_desc& d, int chunks, bool with_bwd) {
@@ -99,18 +147,25 @@ int setup(const scan2d_desc& d, int chunks, bool with_bwd) {
         cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming) != cudaSuccess)
       return SCAN2D_ECUDA;
   if (cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess) return SCAN2D_ECUDA;
+  c->sched = schedule(d.num_scans, chunks, c->chunk_scans);
   scan2d_desc cd = d;
   cd.num_scans = c->chunk_scans;
   cd.params_period = c->chunk_scans;
   cd.bc_group = 1;
   const size_t es = es_of(d.dtype);
-  size_t in[8], out[8];
+  const size_t S = static_cast<size_t>(d.num_scans), N = static_cast<size_t>(d.state_dim);
+  const size_t pc[3] = {S * N, S, S};
+  for (int i = 0; i < 3; ++i) {
+    if (cudaMalloc(&c->par[i], pc[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
+    if (with_bwd && cudaMalloc(&c->dpar[i], pc[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
+  }
+  size_t in[kIn], out[kOut];
   counts(d, c->chunk_scans, in, out);
   for (Slot& s : c->slot) {
-    for (int i = 0; i < 8; ++i) {
-      if (cudaMalloc(&s.in[i], in[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
+    for (int i = 0; i < kIn; ++i)
+      if ((with_bwd || i < 4) && cudaMalloc(&s.in[i], in[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
+    for (int i = 0; i < kOut; ++i)
       if ((with_bwd || i == 0) && cudaMalloc(&s.out[i], out[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
-    }
     s.wsf_bytes = scan2d_workspace_bytes(&cd, SCAN2D_OP_FWD);
     if (cudaMalloc(&s.wsf, s.wsf_bytes) != cudaSuccess) return SCAN2D_ENOMEM;
     if (with_bwd) {
@@ -135,11 +190,12 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
   if (!x || !z || !B || !C || !A || !Dskip || !bias || !y) return SCAN2D_EINVAL;
   const bool bwd = dy != nullptr;
   if (bwd && (!dx || !dz || !dA || !dB || !dC || !dDskip || !dbias)) return SCAN2D_EINVAL;
+  const size_t es = es_of(d.dtype);
   if (chunks < 1) {  // auto: >= 32 MB of host->device traffic per chunk, at most 8 chunks
-    size_t in[8], out[8];
+    size_t in[kIn], out[kOut];
     counts(d, d.num_scans, in, out);
     size_t bytes = 0;
-    for (int i = 0; i < 8; ++i) bytes += in[i] * es_of(d.dtype);
+    for (int i = 0; i < kIn; ++i) bytes += in[i] * es;
     chunks = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, bytes / (32u << 20))));
   }
   if (chunks > d.num_scans) chunks = static_cast<int>(d.num_scans);
@@ -149,23 +205,29 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
   if (rc != SCAN2D_OK) return rc;
   Ctx& c = *g_ctx;
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-  const size_t es = es_of(d.dtype);
-  const void* hin[8] = {x, z, B, C, A, Dskip, bias, dy};
-  void* hout[8] = {y, dx, dz, dA, dB, dC, dDskip, dbias};
+  const size_t N = static_cast<size_t>(d.state_dim);
+  const size_t pc[3] = {static_cast<size_t>(d.num_scans) * N, static_cast<size_t>(d.num_scans),
+                        static_cast<size_t>(d.num_scans)};
+  const void* hpar[3] = {A, Dskip, bias};
+  void* hdpar[3] = {dA, dDskip, dbias};
+  const void* hin[kIn] = {x, z, B, C, dy};
+  void* hout[kOut] = {y, dx, dz, dB, dC};
   // everything starts after the work already on the caller's stream
   if (cudaEventRecord(c.ev_start, user) != cudaSuccess) return SCAN2D_ECUDA;
   cudaStreamWaitEvent(c.h2d, c.ev_start, 0);
-  const int nchunk = static_cast<int>((d.num_scans + c.chunk_scans - 1) / c.chunk_scans);
+  for (int i = 0; i < 3; ++i)
+    if (cudaMemcpyAsync(c.par[i], hpar[i], pc[i] * es, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
+      return SCAN2D_ECUDA;
+  const int nchunk = static_cast<int>(c.sched.size());
   for (int k = 0; k < nchunk; ++k) {
     const int sl = k % Ctx::kSlots;
     Slot& s = c.slot[sl];
-    const int64_t s0 = static_cast<int64_t>(k) * c.chunk_scans;
-    const int64_t sk = std::min<int64_t>(c.chunk_scans, d.num_scans - s0);
-    size_t in[8], out[8], in0[8], out0[8];
+    const int64_t s0 = c.sched[k].first, sk = c.sched[k].second;
+    size_t in[kIn], out[kOut], in0[kIn], out0[kOut];
     counts(d, sk, in, out);
     counts(d, s0, in0, out0);  // element offsets of this chunk in the host arrays
     if (k >= Ctx::kSlots) cudaStreamWaitEvent(c.h2d, c.ev_free[sl], 0);
-    for (int i = 0; i < (bwd ? 8 : 7); ++i)
+    for (int i = 0; i < (bwd ? kIn : 4); ++i)
       if (cudaMemcpyAsync(s.in[i], static_cast<const char*>(hin[i]) + in0[i] * es, in[i] * es,
                           cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
         return SCAN2D_ECUDA;
@@ -174,26 +236,34 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
     scan2d_desc cd = d;
     cd.num_scans = sk;
     cd.params_period = static_cast<int32_t>(sk);
-    rc = scan2d_forward(&cd, s.in[0], s.in[1], s.in[2], s.in[3], s.in[4], s.in[5], s.in[6], s.out[0], nullptr,
-                        nullptr, bwd ? s.residual : nullptr, s.wsf, s.wsf_bytes,
-                        reinterpret_cast<scan2d_stream_t>(c.comp));
+    const char* pA = static_cast<const char*>(c.par[0]) + s0 * N * es;
+    const char* pD = static_cast<const char*>(c.par[1]) + s0 * es;
+    const char* pb = static_cast<const char*>(c.par[2]) + s0 * es;
+    rc = scan2d_forward(&cd, s.in[0], s.in[1], s.in[2], s.in[3], pA, pD, pb, s.out[0], nullptr, nullptr,
+                        bwd ? s.residual : nullptr, s.wsf, s.wsf_bytes, reinterpret_cast<scan2d_stream_t>(c.comp));
     if (rc != SCAN2D_OK) return rc;
     if (bwd) {
-      rc = scan2d_backward(&cd, s.in[0], s.in[1], s.in[2], s.in[3], s.in[4], s.in[5], s.in[6], s.residual,
-                           s.in[7], s.out[1], s.out[2], s.out[3], s.out[4], s.out[5], s.out[6], s.out[7], s.wsb,
-                           s.wsb_bytes, reinterpret_cast<scan2d_stream_t>(c.comp));
+      rc = scan2d_backward(&cd, s.in[0], s.in[1], s.in[2], s.in[3], pA, pD, pb, s.residual, s.in[4], s.out[1],
+                           s.out[2], static_cast<char*>(c.dpar[0]) + s0 * N * es, s.out[3], s.out[4],
+                           static_cast<char*>(c.dpar[1]) + s0 * es, static_cast<char*>(c.dpar[2]) + s0 * es,
+                           s.wsb, s.wsb_bytes, reinterpret_cast<scan2d_stream_t>(c.comp));
       if (rc != SCAN2D_OK) return rc;
     }
     cudaEventRecord(c.ev_out[sl], c.comp);
     cudaStreamWaitEvent(c.d2h, c.ev_out[sl], 0);
-    for (int i = 0; i < (bwd ? 8 : 1); ++i)
+    for (int i = 0; i < (bwd ? kOut : 1); ++i)
       if (cudaMemcpyAsync(static_cast<char*>(hout[i]) + out0[i] * es, s.out[i], out[i] * es,
                           cudaMemcpyDeviceToHost, c.d2h) != cudaSuccess)
         return SCAN2D_ECUDA;
     cudaEventRecord(c.ev_free[sl], c.d2h);
   }
-  // the caller's stream resumes after the last device -> host copy
-  for (int k = std::max(0, nchunk - Ctx::kSlots); k < nchunk; ++k)
-    cudaStreamWaitEvent(user, c.ev_free[k % Ctx::kSlots], 0);
+  // parameter gradients: once, after the last chunk's kernels (d2h is ordered after them)
+  if (bwd)
+    for (int i = 0; i < 3; ++i)
+      if (cudaMemcpyAsync(hdpar[i], c.dpar[i], pc[i] * es, cudaMemcpyDeviceToHost, c.d2h) != cudaSuccess)
+        return SCAN2D_ECUDA;
+  if (cudaEventRecord(c.ev_start, c.d2h) != cudaSuccess) return SCAN2D_ECUDA;
+  // the caller's stream resumes after the last device -> host copy (d2h is in order)
+  cudaStreamWaitEvent(user, c.ev_start, 0);
   return cudaGetLastError() == cudaSuccess ? SCAN2D_OK : SCAN2D_ECUDA;
 }
