@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libscan2d_cuda.so")
+LIB_PATH = os.environ.get("SCAN2D_LIB_PATH") or os.path.join(_PKG, "lib", "libscan2d_cuda.so")
 
 OK, EINVAL, ESTALE, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4, 5
 F32, F64 = 0, 1
