@@ -314,11 +314,7 @@ def main():
 
     import torch
 
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, local = init_dist(torch, world, local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2412_00678_b200.api import Scan2dOp
@@ -378,9 +374,7 @@ def main():
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in evs)
     bwd_ms = statistics.mean(b.elapsed_time(c) for _, b, c in evs) if wl["bwd"] else 0.0
     if dist is not None:
-        t = torch.tensor([total_ms, fwd_ms, bwd_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, fwd_ms, bwd_ms = [float(v) for v in t.tolist()]
+        total_ms, fwd_ms, bwd_ms = max_over_ranks(torch, dist, dev, [total_ms, fwd_ms, bwd_ms])
     sampler.stop()
     clocks = sampler.summary(t_host0, t_host1)
     ms_per_step = total_ms / args.steps
@@ -434,9 +428,7 @@ def main():
         torch.cuda.synchronize()
         e_ms = ea.elapsed_time(eb) / k2
         if dist is not None:
-            t = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            (e_ms,) = max_over_ranks(torch, dist, dev, [e_ms])
         e2e = {"value": elems / (e_ms * 1e-3) / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": k2, "chunks": args.e2e_chunks,
                "path": "C ABI scan2d_train_host: pinned host operands, H2D / kernels / D2H pipelined over "
@@ -460,6 +452,29 @@ def main():
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def init_dist(torch, world, local):
+    """One process per GPU over NCCL.  SCAN2D_BENCH_SHARED_GPU=1 is a test hook
+    for one-GPU boxes: every rank uses cuda:0 and the timing collectives go over
+    gloo (NCCL refuses two ranks on one device); numbers from it are not bench
+    values."""
+    if world <= 1:
+        return None, local
+    import torch.distributed as dist
+
+    if os.environ.get("SCAN2D_BENCH_SHARED_GPU") == "1":
+        dist.init_process_group("gloo")
+        return dist, 0
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist, local
+
+
+def max_over_ranks(torch, dist, dev, vals):
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([float(v) for v in vals], device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
 
 
 def rowband_main(args, wl, rank, world, local, config):
