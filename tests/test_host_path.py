@@ -9,7 +9,8 @@ from scan_cases import batch_to_torch, make_batch, oracle_bwd, oracle_fwd
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shape,chunks", [((10, 24, 40, 16), 3), ((9, 14, 14, 1), 4), ((5, 20, 32, 8), 1)])
+@pytest.mark.parametrize("shape,chunks", [((10, 24, 40, 16), 3), ((9, 14, 14, 1), 4), ((5, 20, 32, 8), 1),
+                                         ((40, 12, 24, 16), 3), ((33, 8, 16, 16), 2)])  # last two: ramped ends
 def test_train_host_matches_device_path(shape, chunks):
     from paper_2412_00678_b200.api import Scan2dOp, train_host
 

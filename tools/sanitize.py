@@ -22,7 +22,12 @@ for (S, H, W, N) in [(2, 9, 40, 16), (3, 9, 212, 16), (2, 6, 40, 4), (2, 5, 20, 
         op.backward(x, z, B, C, A, D, bias, dy)
         torch.cuda.synchronize()
         print("ok", S, H, W, N, dt, flush=True)
-hin = [t.cpu().pin_memory() for t in (x, z, B, C, A, D, bias)]
-train_host(*hin, dy=dy.cpu().pin_memory(), chunks=2)
+g = torch.Generator(device=dev).manual_seed(2)
+S, H, W, N = 33, 8, 16, 16  # two chunks of 17 / 16 scans, ends split into 1/8,1/8,1/4,1/2 pieces
+r = lambda *s: torch.randn(*s, generator=g, device=dev)
+hin = [t.cpu().pin_memory() for t in (r(S, H, W), r(S, H, W), r(S, H, W, N), r(S, H, W, N),
+                                      -(0.05 + 0.9 * torch.rand(S, N, generator=g, device=dev)), r(S),
+                                      torch.rand(S, generator=g, device=dev) - 0.5)]
+train_host(*hin, dy=r(S, H, W).cpu().pin_memory(), chunks=2)
 torch.cuda.synchronize()
 print("ok host path")
