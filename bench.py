@@ -384,11 +384,18 @@ def main():
     fb, bb = alg_bytes(wl)
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.workload)
-    tile = op.plan()["cols_per_chunk"] == 1 and wl["N"] in (4, 8, 16, 32)
-    if wl["bwd"]:
-        dom_name, dom_bytes, dom_ms = ("scan2d_bwd_tile2_kernel" if tile else "scan2d_bwd_kernel"), bb, bwd_ms
+    # kernel family the library picks (scan2d_capi.cu: rows1_shape, use_tile_*)
+    if wl["N"] == 1 and wl["W"] <= 128:
+        family = "rows1"
+    elif op.plan()["cols_per_chunk"] == 1 and wl["N"] in (4, 8, 16, 32):
+        family = "tile2"
     else:
-        dom_name, dom_bytes, dom_ms = ("scan2d_fwd_tile2_kernel" if tile else "scan2d_fwd_kernel"), fb, fwd_ms
+        family = None
+    kname = lambda d: f"scan2d_{d}_{family}_kernel" if family else f"scan2d_{d}_kernel"
+    if wl["bwd"]:
+        dom_name, dom_bytes, dom_ms = kname("bwd"), bb, bwd_ms
+    else:
+        dom_name, dom_bytes, dom_ms = kname("fwd"), fb, fwd_ms
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src, "frac_of_nominal_8000": achieved / 8000.0,

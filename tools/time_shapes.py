@@ -1,4 +1,4 @@
-"""Time forward (training, residual saved) and backward for arbitrary shapes.
+"""Time forward (training, residual saved; and inference) and backward for arbitrary shapes.
 
 usage: python tools/time_shapes.py S,H,W,N[,G] ...   (fp32, CUDA events, inputs resident;
 G = scans sharing one B/C block, the model.cpp layout)
@@ -38,12 +38,19 @@ def run(S, H, W, N, G=1, reps=10):
         torch.cuda.synchronize()
         tf += ev[0].elapsed_time(ev[1])
         tb += ev[1].elapsed_time(ev[2])
-    tf, tb = tf / reps, tb / reps
+    ti = 0.0
+    for _ in range(reps):  # inference forward (no residual)
+        ev[0].record()
+        op.forward(*ins, save=False)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ti += ev[0].elapsed_time(ev[1])
+    tf, tb, ti = tf / reps, tb / reps, ti / reps
     # per-scan B/C (G = 1): memsim.cpp:45-46; shared B/C: B/C bytes once per group
     cells = H * W * 4
     fb = cells * (3 * S + 2 * N * (S // G))
     bb = cells * (5 * S + 4 * N * (S // G))
-    return {"shape": [S, H, W, N, G], "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4),
+    return {"shape": [S, H, W, N, G], "fwd_ms": round(tf, 4), "fwd_infer_ms": round(ti, 4), "bwd_ms": round(tb, 4),
             "fwd_gbs": round(fb / tf / 1e6, 1), "bwd_gbs": round(bb / tb / 1e6, 1), "plan_f": op.plan()}
 
 
