@@ -2,7 +2,8 @@
 
 The library is built in-tree (``make -C paper_2412_00678_b200/csrc``, or
 ``__graft_entry__.build()``).  There is no CPU fallback: if the shared object is
-missing this module raises at import time.
+missing this module raises at import time.  ``SCAN2D_LIB_PATH`` points the loader
+at another build of the same library (A/B timing of kernel variants).
 """
 from __future__ import annotations
 

@@ -223,3 +223,15 @@ def test_engine_shim_exports_reference_api():
                 "scan2d::tiled_scan_2d_backward<float>", "scan2d::tiled_scan_2d_backward<double>",
                 "scan2d::naive_scan_2d<double>", "scan2d::block_scan_1d_forward<float>"):
         assert sym in out, sym
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: importing the binding without its shared object raises."""
+    import subprocess
+    import sys as _sys
+
+    code = "import paper_2412_00678_b200._native"
+    env = dict(os.environ, SCAN2D_LIB_PATH=str(tmp_path / "missing.so"))
+    p = subprocess.run([_sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True, text=True)
+    assert p.returncode != 0
+    assert "missing.so" in p.stderr or "OSError" in p.stderr
