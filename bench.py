@@ -259,8 +259,13 @@ def parity_vs_reference(cr, dev, max_scans=16):
     t = [torch.from_numpy(np.ascontiguousarray(v)).to(dev) for v in (x, z, B, C, A, D, bias)]
     op = Scan2dOp(k, H, W, N, tile=16, device=dev, with_backward=False)
     y = op.forward(*t, save=False).cpu().numpy()
+    # the reference's own fp32 engine on the same inputs, for scale
+    _, y32 = cr.ref.batch(k, k, 1, H, W, N, 16, cr.threads, False,
+                          *[np.asarray(v, np.float32) for v in (x, z, B, C, A, D, bias)], dtype="f32",
+                          want_y=True)
     return {"scans": k, "against": "reference tiled_scan_2d_forward<double> (oracle/_ref)",
-            "normwise_rel": rel_error(y, y64), "tolerance": 1e-4, "elem_rel": elem_stats(y, y64)}
+            "normwise_rel": rel_error(y, y64), "tolerance": 1e-4, "elem_rel": elem_stats(y, y64),
+            "reference_f32": {"normwise_rel": rel_error(y32, y64), "elem_rel": elem_stats(y32, y64)}}
 
 
 # ----------------------------------------------------------------- main
