@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   T dA_acc[SPL];
 #pragma unroll
   for (int e = 0; e < SPL; ++e) dA_acc[e] = T(0);
-  T dbias_acc = T(0), dD_acc = T(0);
+  // per-cell scalar sums run over the whole strip: accumulate in double
+  double dbias_acc = 0.0, dD_acc = 0.0;
 
   __syncwarp();
   const int njobs = 2 * H;
@@ -406,8 +407,8 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
             const T dzv = ddp[m] * sv;
             dxs[rowb + j] = fma(Dsk, dyv, dv * sgb[m]);
             dzs[rowb + j] = dzv;
-            dbias_acc += dzv;
-            dD_acc = fma(dyv, xv, dD_acc);
+            dbias_acc += static_cast<double>(dzv);
+            dD_acc = fma(static_cast<double>(dyv), static_cast<double>(xv), dD_acc);
           }
         }
       }
@@ -432,8 +433,8 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
         if (e < nvalid) part[q * SPL + e] = dA_acc[e];
     }
     if (lane_in_seg == 0) {
-      part[N] = dbias_acc;
-      part[N + 1] = dD_acc;
+      part[N] = static_cast<T>(dbias_acc);
+      part[N + 1] = static_cast<T>(dD_acc);
     }
   }
 }

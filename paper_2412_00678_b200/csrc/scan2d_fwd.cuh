@@ -150,8 +150,9 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
       has_succ ? a.hcarry + ((sc * nq + ((lm.c0 + ge.colsw) / Q - 1)) * H) * N + q * SPL : nullptr;
   // residual (plain values): the warp's outgoing carry, and the carry-in of a
   // chunk starting on an interior Q boundary
-  T* hr_out = save && has_succ ? a.hres + ((sc * nq + ((lm.c0 + ge.colsw) / Q - 1)) * H) * N + q * SPL : nullptr;
-  const bool chunk_q = save && cis > 0 && (lm.colc % Q) == 0 && lm.colc < W;
+  T* hr_out = save && has_succ && lm.scan_ok ? a.hres + ((sc * nq + ((lm.c0 + ge.colsw) / Q - 1)) * H) * N + q * SPL : nullptr;
+  // (segments past the last scan alias scan 0: they must not write)
+  const bool chunk_q = save && lm.scan_ok && cis > 0 && (lm.colc % Q) == 0 && lm.colc < W;
   T* hr_mid = chunk_q ? a.hres + ((sc * nq + (lm.colc / Q - 1)) * H) * N + q * SPL : nullptr;
   T* yrow = a.y + sc * HW;
 
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
         }
         if (lm.c == CPW - 1) {
           carry_put<T, SPL>(hc_out + static_cast<size_t>(i) * N, out, tag, nvalid);
-          if (save) store_states<T, SPL>(hr_out + static_cast<size_t>(i) * N, out, nvalid);
+          if (hr_out != nullptr) store_states<T, SPL>(hr_out + static_cast<size_t>(i) * N, out, nvalid);
         }
       }
 #pragma unroll

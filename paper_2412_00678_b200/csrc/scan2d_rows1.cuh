@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
 #pragma unroll
   for (int k = 0; k < J; ++k) dn[k] = T(0);
   if (a.gbot != nullptr && ok) ldg_states<T, J>(dn, a.gbot + s * W + q * J);
-  T dA_acc = T(0), db_acc = T(0), dD_acc = T(0);
+  // per-scan scalar sums over every cell: accumulate in double
+  double dA_acc = 0.0, db_acc = 0.0, dD_acc = 0.0;
 
   // job order per band: F rows r0 .. r0+K-1, then R rows r0+K-1 .. r0.  Each
   // lane streams its own columns of the next NJ-1 row-jobs into a private
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
         const T hu = rr > 0 ? hr[rr > 0 ? rr - 1 : 0][k] : hp0[k];
         const T dab = fma(gh, hl, G[k] * hu);  // engine.cpp:383
         const T t = dab * av[k];
-        dA_acc = fma(t, d[k], dA_acc);
+        dA_acc = fma(static_cast<double>(t), static_cast<double>(d[k]), dA_acc);
         const T gb = gh * cur.b[k];
         const T dd = fma(t, Au, gb * cur.x[k]);
         dB[k] = gh * (d[k] * cur.x[k]);
@@ -372,8 +373,8 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
         dx[k] = fma(Dsk, cur.dy[k], d[k] * gb);
         dz[k] = dd * sg[k];
         if (ok && i < H) {
-          db_acc += dz[k];
-          dD_acc = fma(cur.dy[k], cur.x[k], dD_acc);
+          db_acc += static_cast<double>(dz[k]);
+          dD_acc = fma(static_cast<double>(cur.dy[k]), static_cast<double>(cur.x[k]), dD_acc);
         }
       }
       if (ok && i < H) {
@@ -395,14 +396,14 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
   }
   if (q == 0 && id.s < a.S) {
     if (a.fuse) {  // P == S: one warp segment owns the scan -- write the gradients directly
-      a.dA_out[id.s] = dA_acc;
-      a.dbias_out[id.s] = db_acc;
-      a.dD_out[id.s] = dD_acc;
+      a.dA_out[id.s] = static_cast<T>(dA_acc);
+      a.dbias_out[id.s] = static_cast<T>(db_acc);
+      a.dD_out[id.s] = static_cast<T>(dD_acc);
     } else {
       T* part = a.part + static_cast<size_t>(id.s) * 3;  // [S][1][N + 2], N = 1
-      part[0] = dA_acc;
-      part[1] = db_acc;
-      part[2] = dD_acc;
+      part[0] = static_cast<T>(dA_acc);
+      part[1] = static_cast<T>(db_acc);
+      part[2] = static_cast<T>(dD_acc);
     }
   }
 }

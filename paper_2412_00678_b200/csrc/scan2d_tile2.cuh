@@ -675,7 +675,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   T dAr[SH];
 #pragma unroll
   for (int e = 0; e < SH; ++e) dAr[e] = T(0);
-  T dbias_acc = T(0), dD_acc = T(0);
+  // per-cell scalar sums run over the whole strip: accumulate in double
+  double dbias_acc = 0.0, dD_acc = 0.0;
 
   const int ntiles = (H + R - 1) / R;
   int sc = 0;  // slot with C (then G) of this tile; sc+1: hh; sc+2: C of the next tile up
@@ -919,8 +920,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           const T dzv = dd * SGs[c];
           dxg[static_cast<size_t>(i1) * W + j] = fma(Dsk, dyv, dv * sgb[0]);
           dzg[static_cast<size_t>(i1) * W + j] = dzv;
-          dbias_acc += dzv;
-          dD_acc = fma(dyv, xv, dD_acc);
+          dbias_acc += static_cast<double>(dzv);
+          dD_acc = fma(static_cast<double>(dyv), static_cast<double>(xv), dD_acc);
         }
       }
       if (pred_ring)
@@ -960,8 +961,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     for (int e = 0; e < SV; ++e) part[s2 * SV + e] = scr[s2 * SV + e] + dAc[e];
   }
   if (lane == 0) {
-    part[N] = dbias_acc;
-    part[N + 1] = dD_acc;
+    part[N] = static_cast<T>(dbias_acc);
+    part[N + 1] = static_cast<T>(dD_acc);
   }
   if (a.fuse) {  // P == S: the scan's last strip adds the partials, strip order fixed
     bool last = ge.wreal == 1;

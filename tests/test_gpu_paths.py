@@ -113,3 +113,27 @@ def test_state_groups_shared_params():
     got = dict(dx=g.dx, dz=g.dz_raw, dA=g.da, dB=g.db, dC=g.dc, dD=g.dd, dbias=g.dbias)
     for k, t in got.items():
         assert rel_error(t.cpu().numpy().reshape(-1), np.asarray(ref[k]).reshape(-1)) <= F64_G_GATE, k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("S,H,W,N,P,dtype,T", [
+    (6, 77, 20, 4, 3, "f32", 5),     # 4 scans per warp, last warp half empty
+    (1, 24, 30, 4, 1, "f64", 64),    # 2 scans per warp, one empty segment
+    (3, 45, 20, 260, 3, "f64", 16),  # state groups, the N = 4 remainder group
+    (5, 19, 30, 8, 5, "f32", 7),
+])
+def test_emission_forward_then_backward(orc, S, H, W, N, P, dtype, T):
+    """CarryState emission runs the warp forward (several scans per warp for
+    narrow grids) and the residual it saves feeds the tile backward: segments
+    past the last scan must not write the residual's boundary carries (found
+    by tools/stress_random.py)."""
+    from paper_2412_00678_b200 import tiled_scan_2d_backward, tiled_scan_2d_forward
+
+    b = make_batch(orc, S, H, W, N, seed0=9000, dtype=dtype, P=P)
+    (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    for _ in range(3):  # the failure was a race between segments: repeat
+        res = tiled_scan_2d_forward(x, z, B, C, A, D, bias, tile=T, carries=True)
+        g = tiled_scan_2d_backward(res.saved, dy)
+        torch.cuda.synchronize()
+        _check(orc, b, res.y, [g.dx, g.dz_raw, g.da, g.db, g.dc, g.dd, g.dbias], dtype,
+               f"emit S={S} {H}x{W} N={N} {dtype} T={T}")

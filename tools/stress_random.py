@@ -1,0 +1,88 @@
+"""Long randomised parity sweep on the GPU (not part of the pytest suite):
+forward + backward (+ CarryState emission on a share of the cases) against the
+fp64 oracle over shapes wider than tests/test_gpu_random.py covers.
+
+usage: python tools/stress_random.py <n_cases> [seed] [case,case,... [reps]]
+(the optional list re-runs only those case indices, reps times each).
+Prints one line per failure and a summary; exit code 1 if any case fails.  An
+fp32 result over the gate but within 1.5x of the reference's own fp32 error
+(the oracle restates its arithmetic) is reported as a note, not a failure."""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+from oracle_lib import Oracle, rel_error  # noqa: E402
+from scan_cases import batch_to_torch, make_batch, oracle_bwd, oracle_fwd  # noqa: E402
+from paper_2412_00678_b200 import tiled_scan_2d_backward, tiled_scan_2d_forward  # noqa: E402
+
+
+def cases(n, seed):
+    rng = np.random.default_rng(seed)
+    for _ in range(n):
+        N = int(rng.choice([1, 1, 1, 2, 4, 5, 8, 16, 16, 16, 32, 33, 64, 100, 128, 129, 260]))
+        H = int(rng.integers(1, 90))
+        wmax = 420 if N <= 32 else (130 if N <= 128 else 40)
+        W = int(rng.integers(1, wmax))
+        G = int(rng.choice([1, 1, 1, 2, 3]))
+        P_div = int(rng.choice([1, 1, 2]))
+        S = G * P_div * int(rng.integers(1, 4))
+        dt = str(rng.choice(["f32", "f32", "f64"]))
+        T = int(rng.choice([16, 16, 5, 64]))
+        yield S, H, W, N, S // P_div, G, dt, T
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 7
+    only = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
+    reps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+    orc = Oracle()
+    fails, t0 = 0, time.time()
+    todo = [(k, c) for k, c in enumerate(cases(n, seed)) if only is None or k in only]
+    for k, (S, H, W, N, P, G, dt, T) in [kc for kc in todo for _ in range(reps)]:
+        label = f"#{k} S={S} {H}x{W} N={N} P={P} G={G} {dt} T={T}"
+        try:
+            b = make_batch(orc, S, H, W, N, seed0=9000 + 31 * k, dtype=dt, P=P, G=G)
+            (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+            res = tiled_scan_2d_forward(x, z, B, C, A, D, bias, tile=T, carries=(k % 5 == 0))
+            g = tiled_scan_2d_backward(res.saved, dy)
+            torch.cuda.synchronize()
+            yg, gg = (1e-12, 1e-10) if dt == "f64" else (1e-4, 1e-4)
+            errs = {"y": rel_error(res.y.cpu().numpy(), oracle_fwd(orc, b, "f64"))}
+            ref = oracle_bwd(orc, b, "f64")
+            got = dict(dx=g.dx, dz=g.dz_raw, dA=g.da, dB=g.db, dC=g.dc, dD=g.dd, dbias=g.dbias)
+            for key, t in got.items():
+                errs[key] = rel_error(t.cpu().numpy().reshape(-1), np.asarray(ref[key]).reshape(-1))
+            bad = {k2: v for k2, v in errs.items() if v > (yg if k2 == "y" else gg) or not np.isfinite(v)}
+            if bad:
+                # the reference's own fp32 arithmetic (the oracle restates it) on the same case
+                ref32 = {}
+                if dt == "f32":
+                    r32 = oracle_bwd(orc, b, "f32")
+                    y32 = oracle_fwd(orc, b, "f32")
+                    ref64y = oracle_fwd(orc, b, "f64")
+                    for k2 in bad:
+                        ref32[k2] = (rel_error(y32, ref64y) if k2 == "y" else
+                                     rel_error(np.asarray(r32[k2]).reshape(-1), np.asarray(ref[k2]).reshape(-1)))
+                # fp32 scalar sums over large grids can miss 1e-4 in the reference
+                # itself: only a result worse than the reference's own fp32 fails
+                real = {k2: v for k2, v in bad.items() if not (k2 in ref32 and v <= 1.5 * ref32[k2])}
+                tag = "FAIL" if real else "note (within the reference's fp32 error)"
+                fails += 1 if real else 0
+                print(tag, label, {k2: f"{v:.2e}" for k2, v in bad.items()},
+                      "ref-f32:", {k2: f"{v:.2e}" for k2, v in ref32.items()}, flush=True)
+        except Exception as exc:  # noqa: BLE001
+            fails += 1
+            print("ERROR", label, repr(exc)[:200], flush=True)
+    print(f"stress: {n} cases, {fails} failures, {time.time() - t0:.0f} s", flush=True)
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
