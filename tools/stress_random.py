@@ -1,6 +1,7 @@
 """Long randomised parity sweep on the GPU (not part of the pytest suite):
 forward + backward (+ CarryState emission on a share of the cases) against the
-fp64 oracle over shapes wider than tests/test_gpu_random.py covers.
+fp64 oracle over shapes wider than tests/test_gpu_random.py covers; every
+fourth case runs on operands shifted one element off 16-byte alignment.
 
 usage: python tools/stress_random.py <n_cases> [seed] [case,case,... [reps]]
 (the optional list re-runs only those case indices, reps times each).
@@ -50,6 +51,13 @@ def main():
         try:
             b = make_batch(orc, S, H, W, N, seed0=9000 + 31 * k, dtype=dt, P=P, G=G)
             (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+            if k % 4 == 1:  # misaligned operands (one element off): the non-vector load paths
+                def shift(t):
+                    buf = torch.empty(t.numel() + 1, dtype=t.dtype, device=t.device)
+                    v = buf[1:].view(t.shape)
+                    v.copy_(t)
+                    return v
+                x, z, B, C, dy = [shift(t) for t in (x, z, B, C, dy)]
             res = tiled_scan_2d_forward(x, z, B, C, A, D, bias, tile=T, carries=(k % 5 == 0))
             g = tiled_scan_2d_backward(res.saved, dy)
             torch.cuda.synchronize()
