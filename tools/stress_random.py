@@ -4,6 +4,7 @@ fp64 oracle over shapes wider than tests/test_gpu_random.py covers; every
 fourth case runs on operands shifted one element off 16-byte alignment.
 
 usage: python tools/stress_random.py <n_cases> [seed] [case,case,... [reps]]
+       python tools/stress_random.py big        (a fixed list of large shapes)
 (the optional list re-runs only those case indices, reps times each).
 Prints one line per failure and a summary; exit code 1 if any case fails.  An
 fp32 result over the gate but within 1.5x of the reference's own fp32 error
@@ -38,7 +39,19 @@ def cases(n, seed):
         yield S, H, W, N, S // P_div, G, dt, T
 
 
+BIG = [  # (S, H, W, N, P, G, dtype, T): long chains, many CTAs, wide state, many scans
+    (2, 300, 2000, 16, 2, 1, "f32", 16), (1, 2000, 300, 8, 1, 1, "f32", 16), (3, 64, 4000, 4, 3, 1, "f32", 16),
+    (1, 96, 100, 2048, 1, 1, "f32", 16), (4096, 8, 8, 1, 4096, 1, "f32", 16), (20000, 3, 5, 2, 20000, 1, "f32", 16),
+    (2, 500, 1030, 32, 2, 1, "f64", 16), (6, 256, 520, 16, 3, 2, "f32", 16), (1, 4096, 64, 16, 1, 1, "f32", 16),
+    (300, 40, 129, 1, 300, 1, "f32", 16), (2, 130, 700, 64, 2, 1, "f32", 16), (1, 77, 3001, 16, 1, 1, "f64", 16),
+]
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "big":
+        global cases
+        cases = lambda n, seed: iter(BIG)  # noqa: E731
+        sys.argv[1:2] = [str(len(BIG))]
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 7
     only = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
