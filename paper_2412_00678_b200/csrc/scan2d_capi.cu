@@ -160,7 +160,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p = Plan{};
   p.b = make_geo(d, true);
   p.f = make_geo(d, false);
-  p.pfd = env_int("SCAN2D_ROWS1_PFD", 8);
+  p.pfd = env_int("SCAN2D_ROWS1_PFD", 6);  // measured: 6 rows ahead best on cfg3 / cfg4a (4..12, 1000 = off)
   if (rows1_shape(d)) {
     p.K = 4;
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
