@@ -33,9 +33,10 @@
 //    in scan-major order; neighbouring strips of one scan in one CTA pass the
 //    horizontal carry through an mbarrier-guarded shared-memory ring, strips in
 //    different CTAs through tagged 8-byte words in global memory (CTA tickets
-//    keep producers resident).  The forward publishes hh at every strip
-//    boundary (kept as the training residual) and h at the last row of every
-//    tile (checkpoints), so the backward recomputes instead of storing states.
+//    keep producers resident).  A training forward also stores hh at every
+//    strip boundary (plain values, residual `hres`) and h at the last row of
+//    every tile (checkpoints), so the backward recomputes instead of storing
+//    states.
 // Shared memory per warp (fp32, N = 16): 14.3 KB forward, 16.5 KB backward.
 #pragma once
 
