@@ -88,12 +88,11 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   const int nvalid = N - q * SPL;
   const bool svec = nvalid >= SPL && (N % SPL) == 0;  // vector global stores of the lane's states
 
-  T A2[SPL], Ad[SPL];
+  T Ad[SPL];  // natural units: Abar = exp_nat(delta A)
 #pragma unroll
   for (int e = 0; e < SPL; ++e) {
     const int d = q * SPL + e;
     Ad[e] = (lm.scan_ok && d < N) ? a.A[static_cast<int64_t>(p) * N + d] : T(0);
-    A2[e] = Num<T>::a_scale(Ad[e]);
   }
   const T Dsk = a.Dskip[p], bias = a.bias[p];
 
@@ -198,7 +197,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
       lds_states<T, SPL>(bq, sx + Ls.bo + col * Np + q * SPL, true);
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
-        av[k][e] = Num<T>::exp_scaled(delta[k] * A2[e]);
+        av[k][e] = Num<T>::exp_nat(delta[k] * Ad[e]);
         uv[k][e] = (delta[k] * bq[e]) * xk;
       }
     }

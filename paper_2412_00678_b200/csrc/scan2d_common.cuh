@@ -28,6 +28,16 @@ struct Num<float> {
     return r;
   }
   static __device__ __forceinline__ float a_scale(float a) { return a * 1.4426950408889634f; }
+  // exp(x) for natural x with the rounding of x log2 e and the low part of
+  // log2 e folded back: no per-state systematic bias from a pre-rounded
+  // A log2 e (the general warp kernels, where N can reach 128 states and
+  // that bias adds up coherently in the per-scan dbias sum)
+  static __device__ __forceinline__ float exp_nat(float x) {
+    const float t = x * 1.44269502162933349609375f;
+    const float e = fmaf(x, 1.44269502162933349609375f, -t) + x * 1.925963033500011079e-8f;
+    const float r = exp_scaled(t);
+    return fmaf(r, e * 0.6931471805599453f, r);
+  }
   static __device__ __forceinline__ float rcp(float v) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
@@ -62,6 +72,7 @@ template <>
 struct Num<double> {
   static __device__ __forceinline__ double exp_scaled(double x) { return exp(x); }
   static __device__ __forceinline__ double a_scale(double a) { return a; }
+  static __device__ __forceinline__ double exp_nat(double x) { return exp(x); }
   static __device__ __forceinline__ double softplus(double v) {
     return v > 20.0 ? v : log1p(exp(v));
   }

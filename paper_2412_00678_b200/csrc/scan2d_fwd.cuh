@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
 #pragma unroll
   for (int e = 0; e < SPL; ++e) {
     const int d = q * SPL + e;
-    A2[e] = (lm.scan_ok && d < N) ? Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + d]) : T(0);
+    A2[e] = (lm.scan_ok && d < N) ? a.A[static_cast<int64_t>(p) * N + d] : T(0);  // natural units (exp_nat)
   }
   const T Dsk = a.Dskip[p], bias = a.bias[p];
 
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
       const T dx = delta[k];
 #pragma unroll
       for (int e = 0; e < SPL; ++e) {
-        av[k][e] = Num<T>::exp_scaled(dx * A2[e]);
+        av[k][e] = Num<T>::exp_nat(dx * A2[e]);
         uv[k][e] = (dx * bq[e]) * xk;
         if (k == 0) {
           Pc[e] = av[k][e];
