@@ -246,6 +246,8 @@ class Scan2dOp:
     def __init__(self, S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=torch.float32,
                  device="cuda", with_backward=True):
         self.dev = torch.device(device)
+        if self.dev.type == "cuda" and self.dev.index is None:
+            self.dev = torch.device("cuda", torch.cuda.current_device())
         self.dtype = dtype
         code = nat.F64 if dtype == torch.float64 else nat.F32
         self.desc = nat.make_desc(S, H, W, N, tile=tile, params_period=params_period, bc_group=bc_group,
@@ -270,8 +272,27 @@ class Scan2dOp:
             self.dB, self.dC = e(G, H, W, N), e(G, H, W, N)
             self.dA, self.dD, self.dbias = e(P, N), e(P), e(P)
         self.launches = 0
+        self.check = True  # validate operands against the descriptor (benchmarks may turn it off)
+
+    def _operands(self, x, z, B, C_, A, Dskip, bias, dy=None):
+        """Shape / dtype / device / contiguity of every operand against the
+        preallocated descriptor: a raw pointer goes to the C ABI, so a view or
+        a wrong dtype would otherwise be read out of bounds silently."""
+        S, H, W, N, P, G = self.shape
+        want = [("x", x, (S, H, W)), ("z", z, (S, H, W)), ("B", B, (G, H, W, N)), ("C", C_, (G, H, W, N)),
+                ("A", A, (P, N)), ("Dskip", Dskip, (P,)), ("bias", bias, (P,))]
+        if dy is not None:
+            want.append(("dy", dy, (S, H, W)))
+        for name, t, shp in want:
+            _check(isinstance(t, torch.Tensor), f"Scan2dOp: {name} must be a tensor")
+            _check(tuple(t.shape) == shp, f"Scan2dOp: {name} has shape {tuple(t.shape)}, expected {shp}")
+            _check(t.dtype == self.dtype, f"Scan2dOp: {name} has dtype {t.dtype}, expected {self.dtype}")
+            _check(t.device == self.dev, f"Scan2dOp: {name} is on {t.device}, expected {self.dev}")
+            _check(t.is_contiguous(), f"Scan2dOp: {name} must be contiguous")
 
     def forward(self, x, z, B, C_, A, Dskip, bias, save=True):
+        if self.check:
+            self._operands(x, z, B, C_, A, Dskip, bias)
         rc = nat.lib.scan2d_forward(C.byref(self.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A), _ptr(Dskip),
                                     _ptr(bias), _ptr(self.y), None, None,
                                     _ptr(self.residual) if save else None, _ptr(self.wsf), self.wsf_bytes,
@@ -282,6 +303,8 @@ class Scan2dOp:
         return self.y
 
     def backward(self, x, z, B, C_, A, Dskip, bias, dy):
+        if self.check:
+            self._operands(x, z, B, C_, A, Dskip, bias, dy)
         rc = nat.lib.scan2d_backward(C.byref(self.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
                                      _ptr(Dskip), _ptr(bias), _ptr(self.residual), _ptr(dy), _ptr(self.dx),
                                      _ptr(self.dz), _ptr(self.dA), _ptr(self.dB), _ptr(self.dC), _ptr(self.dD),
@@ -338,8 +361,18 @@ class Scan2dBandOp:
     def desc(self):
         return self.op.desc
 
+    def _carry(self, t, name):
+        if t is not None:
+            S, H, W, N, _, _ = self.op.shape
+            _check(tuple(t.shape) == (S, W, N) and t.dtype == self.op.dtype and t.device == self.op.dev
+                   and t.is_contiguous(), f"Scan2dBandOp: {name} must be a contiguous [S,W,N] tensor "
+                                          "of the op's dtype on its device")
+
     def forward(self, x, z, B, C_, A, Dskip, bias, h_top=None, save=True):
         o = self.op
+        if o.check:
+            o._operands(x, z, B, C_, A, Dskip, bias)
+            self._carry(h_top, "h_top")
         rc = nat.lib.scan2d_forward_band(C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
                                          _ptr(Dskip), _ptr(bias), _ptr(h_top), _ptr(o.y), _ptr(self.h_bottom),
                                          _ptr(o.residual) if save else None, _ptr(o.wsf), o.wsf_bytes,
@@ -351,6 +384,10 @@ class Scan2dBandOp:
 
     def backward(self, x, z, B, C_, A, Dskip, bias, h_top, dy, g_bottom=None):
         o = self.op
+        if o.check:
+            o._operands(x, z, B, C_, A, Dskip, bias, dy)
+            self._carry(h_top, "h_top")
+            self._carry(g_bottom, "g_bottom")
         rc = nat.lib.scan2d_backward_band(C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
                                           _ptr(Dskip), _ptr(bias), _ptr(h_top), _ptr(o.residual), _ptr(dy),
                                           _ptr(g_bottom), _ptr(o.dx), _ptr(o.dz), _ptr(o.dA), _ptr(o.dB),
@@ -362,23 +399,47 @@ class Scan2dBandOp:
         return o.dx, o.dz, o.dA, o.dB, o.dC, o.dD, o.dbias, self.g_top
 
 
-def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 0, tile: int = 16):
+def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 0, tile: int = 16,
+               sync: bool = True):
     """One training step with HOST (CPU, ideally pinned) tensors through the C
     ABI's ``scan2d_train_host``: chunked host->device copies, kernels and
     device->host copies overlap on three streams of the current device.
     Returns ``outs`` = (y, dx, dz, dA, dB, dC, dD, dbias) as host tensors
-    (gradients None when ``dy`` is None).  Per-scan parameters and B/C only."""
+    (gradients None when ``dy`` is None).  Per-scan parameters and B/C only
+    (A [S,N], Dskip / bias [S]).  With ``sync=False`` the call returns as soon
+    as the work is enqueued and the outputs are valid only after
+    ``torch.cuda.current_stream().synchronize()``."""
+    _check(x.dim() == 3, "train_host: x must be [S,H,W]")
     S, H, W = x.shape
+    _check(B.dim() == 4, "train_host: B must be [S,H,W,N]")
     N = B.shape[-1]
+    ins = [("x", x, (S, H, W)), ("z", z, (S, H, W)), ("B", B, (S, H, W, N)), ("C", C_, (S, H, W, N)),
+           ("A", A, (S, N)), ("Dskip", Dskip, (S,)), ("bias", bias, (S,))]
+    if dy is not None:
+        ins.append(("dy", dy, (S, H, W)))
+    _check(x.dtype in (torch.float32, torch.float64), "train_host: dtype must be float32 or float64")
+    for name, t, shp in ins:
+        _check(tuple(t.shape) == shp, f"train_host: {name} has shape {tuple(t.shape)}, expected {shp}")
+        _check(t.dtype == x.dtype, f"train_host: {name} must be {x.dtype}")
+        _check(t.device.type == "cpu", f"train_host: {name} must be a host tensor")
+        _check(t.is_contiguous(), f"train_host: {name} must be contiguous")
     code = nat.F64 if x.dtype == torch.float64 else nat.F32
     desc = nat.make_desc(S, H, W, N, tile=tile, dtype=code)
     if outs is None:
         e = lambda *s: torch.empty(s, dtype=x.dtype).pin_memory()
         outs = (e(S, H, W),) + ((e(S, H, W), e(S, H, W), e(S, N), e(S, H, W, N), e(S, H, W, N), e(S), e(S))
                                 if dy is not None else (None,) * 7)
+    oshapes = [(S, H, W), (S, H, W), (S, H, W), (S, N), (S, H, W, N), (S, H, W, N), (S,), (S,)]
+    for k, (t, shp) in enumerate(zip(outs, oshapes)):
+        if k > 0 and dy is None:
+            continue
+        _check(t is not None and tuple(t.shape) == shp and t.dtype == x.dtype and t.device.type == "cpu"
+               and t.is_contiguous(), f"train_host: output {k} must be a contiguous host {shp} tensor")
     dev = torch.device("cuda", torch.cuda.current_device())
     rc = nat.lib.scan2d_train_host(C.byref(desc), *[_ptr(t) for t in (x, z, B, C_, A, Dskip, bias, dy)],
                                    *[_ptr(t) for t in outs], int(chunks), _stream(dev))
     if rc != nat.OK:
         raise nat.Scan2dError(rc, "scan2d_train_host")
+    if sync:
+        torch.cuda.current_stream(dev).synchronize()
     return outs

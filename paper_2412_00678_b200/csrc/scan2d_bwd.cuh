@@ -72,9 +72,13 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   const int K = a.plan.K, nb = a.plan.nb;
 
   int64_t unit = blockIdx.x;
+  const uint32_t epoch = ge.wreal > 1 ? load_epoch(a.hdr) : 0u;
   if (ge.wreal > 1) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1);
+    if (lane == 0) {
+      t = atomicAdd(a.ticket, 1);
+      if (t == 0) a.hdr->magic = a.magic;  // the carry region now follows this layout
+    }
     t = __shfl_sync(kFull, t, 0);
     // reverse order within a scan: the rightmost column group starts first
     const int64_t ss = t / ge.wreal;
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   const int p = static_cast<int>(sc % a.P);
   const size_t HW = static_cast<size_t>(H) * W;
   const int nvalid = N - q * SPL;
-  const bool svec = nvalid >= SPL && (N % SPL) == 0;  // vector global stores of the lane's states
+  const bool svec = a.ovec && nvalid >= SPL && (N % SPL) == 0;  // vector global stores of the lane's states
 
   T Ad[SPL];  // natural units: Abar = exp_nat(delta A)
 #pragma unroll
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
         T rw[SPL];
 #pragma unroll
         for (int e = 0; e < SPL; ++e) rw[e] = T(0);
-        const int tag = row_tag(a.epoch, i);
+        const int tag = row_tag(epoch, i);
         if (has_succ) carry_get_wait<T, SPL>(rc_in + static_cast<size_t>(i) * N, rw, tag, nvalid);
         if (has_pred) {
           T out[SPL];

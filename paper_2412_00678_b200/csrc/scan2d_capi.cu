@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <initializer_list>
 #include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
@@ -393,9 +394,92 @@ ResLayout res_layout(const scan2d_desc& d, const Plan& p) {
   return R;
 }
 
-std::atomic<uint32_t> g_epoch{0x9e3779b9u};
+// Runs before every chained launch, in stream order (captured CUDA graphs
+// replay it too): resets the ticket and the per-scan finish counters, advances
+// the device-side epoch, and -- when the header's magic does not match this
+// launch's layout (fresh or re-purposed memory) -- clears the carry region so
+// that no stale word can carry a valid tag.  Every CTA reads the magic before
+// any writer exists (the main kernel records it), so all agree on `fresh`.
+__global__ void scan2d_begin_kernel(s2d::WsHdr* h, uint32_t magic, uint32_t step, int* cnt, int64_t ncnt,
+                                    uint4* clr, int64_t nclr) {
+  const bool fresh = *reinterpret_cast<volatile uint32_t*>(&h->magic) != magic;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = tid; i < ncnt; i += nth) cnt[i] = 0;
+  if (fresh)
+    for (int64_t i = tid; i < nclr; i += nth) clr[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) {
+    h->ticket = 0;
+    h->epoch = fresh ? 0u : (h->epoch % s2d::kTagSpan + step) % s2d::kTagSpan;
+  }
+}
 
-uint32_t next_epoch(int H) { return g_epoch.fetch_add(static_cast<uint32_t>(H) + 1u); }
+uint32_t fnv(uint32_t hsh, uint64_t v) {
+  for (int i = 0; i < 8; ++i) hsh = (hsh ^ static_cast<uint32_t>((v >> (8 * i)) & 0xff)) * 16777619u;
+  return hsh;
+}
+
+// Layout hash of one chained launch: the descriptor, the op, and every plan
+// field that decides where a carry slot lives.  Never 0 (cleared memory).
+uint32_t layout_magic(const scan2d_desc& d, const Plan& p, int op, size_t carry_off, size_t carry_bytes) {
+  uint32_t hsh = 2166136261u;
+  for (uint64_t v : {static_cast<uint64_t>(d.num_scans), static_cast<uint64_t>(d.height),
+                     static_cast<uint64_t>(d.width), static_cast<uint64_t>(d.state_dim),
+                     static_cast<uint64_t>(d.tile), static_cast<uint64_t>(d.params_period),
+                     static_cast<uint64_t>(d.bc_group), static_cast<uint64_t>(d.dtype),
+                     static_cast<uint64_t>(op), static_cast<uint64_t>(p.f.wreal), static_cast<uint64_t>(p.b.wreal),
+                     static_cast<uint64_t>(p.f.colsw), static_cast<uint64_t>(p.b.colsw),
+                     static_cast<uint64_t>(p.f.tile), static_cast<uint64_t>(p.b.tile),
+                     static_cast<uint64_t>(p.nq), static_cast<uint64_t>(p.Q),
+                     static_cast<uint64_t>(carry_off), static_cast<uint64_t>(carry_bytes)})
+    hsh = fnv(hsh, v);
+  return hsh == 0 ? 1u : hsh;
+}
+
+// Host-side memory of the magic last enqueued per workspace address, so the
+// common case (the same workspace reused with the same layout) launches a
+// single-CTA begin kernel.  The device still checks the magic itself: a wrong
+// guess (the caller overwrote the workspace) costs a slow single-CTA clear,
+// never a wrong result.
+struct MagicCache {
+  static constexpr int kSlots = 64;
+  std::mutex mu;
+  const void* ws[kSlots] = {};
+  uint32_t magic[kSlots] = {};
+  int next = 0;
+  bool seen_and_set(const void* w, uint32_t m) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < kSlots; ++i)
+      if (ws[i] == w) {
+        const bool hit = magic[i] == m;
+        magic[i] = m;
+        return hit;
+      }
+    ws[next] = w;
+    magic[next] = m;
+    next = (next + 1) % kSlots;
+    return false;
+  }
+};
+MagicCache g_magic_cache;
+
+// Enqueue the begin kernel for a chained launch (see scan2d_begin_kernel).
+cudaError_t launch_begin(s2d::WsHdr* h, uint32_t magic, int H, int* cnt, int64_t ncnt, void* clr,
+                         size_t clr_bytes, cudaStream_t st) {
+  uint32_t step = static_cast<uint32_t>(H) + 1u;
+  if (step % s2d::kTagSpan == 0) ++step;
+  step %= s2d::kTagSpan;
+  const int64_t nclr = static_cast<int64_t>(clr_bytes / 16);
+  const int threads = 256;
+  int64_t blocks = 1;
+  if (!g_magic_cache.seen_and_set(h, magic)) {
+    const int64_t work = std::max<int64_t>(ncnt, nclr);
+    blocks = std::max<int64_t>(1, std::min<int64_t>(2 * 148, (work + threads * 8 - 1) / (threads * 8)));
+  }
+  scan2d_begin_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(h, magic, step, cnt, ncnt,
+                                                                          static_cast<uint4*>(clr), nclr);
+  return cudaGetLastError();
+}
 
 int device_check() {
   int dev = 0;
@@ -430,7 +514,6 @@ void fill_common(Args<T>& a, const scan2d_desc& d, const Plan& p, const void* x,
   a.P = d.params_period;
   a.G = d.bc_group;
   a.plan = p;
-  a.epoch = next_epoch(d.height);
 }
 
 template <typename T>
@@ -469,7 +552,8 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   if ((vtop != nullptr || vbot != nullptr) && !p.f.tile) return SCAN2D_EUNSUPPORTED;
   a.vtop = static_cast<const T*>(vtop);
   a.vbot = static_cast<T*>(vbot);
-  a.ticket = reinterpret_cast<int*>(w + L.ticket);
+  a.hdr = reinterpret_cast<s2d::WsHdr*>(w + L.ticket);
+  a.ticket = &a.hdr->ticket;
   if (residual != nullptr) {
     const ResLayout R = res_layout(d, p);
     unsigned char* r = static_cast<unsigned char*>(residual);
@@ -480,8 +564,14 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
     a.hres = nullptr;
   }
   a.hcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.hcarry);
-  if (p.f.wreal > 1 && cudaMemsetAsync(a.ticket, 0, sizeof(int), stream) != cudaSuccess)
-    return SCAN2D_ECUDA;
+  int launches = 0;
+  if (p.f.wreal > 1) {
+    const size_t cb = L.total - L.hcarry;
+    a.magic = layout_magic(d, p, SCAN2D_OP_FWD, L.hcarry, cb);
+    if (launch_begin(a.hdr, a.magic, d.height, nullptr, 0, w + L.hcarry, cb, stream) != cudaSuccess)
+      return SCAN2D_ECUDA;
+    ++launches;
+  }
   if (ph != nullptr) {
     const size_t kh = ceil_div(d.height, d.tile), kw = ceil_div(d.width, d.tile);
     const size_t cb = sizeof(T) * static_cast<size_t>(d.num_scans) * kh * kw * d.tile * d.state_dim;
@@ -489,7 +579,7 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
     if (cudaMemsetAsync(pv, 0, cb, stream) != cudaSuccess) return SCAN2D_ECUDA;
   }
   if (s2d::launch_fwd<T>(a, stream) != cudaSuccess) return SCAN2D_ECUDA;
-  g_last_launches = 1;
+  g_last_launches = launches + 1;
   return SCAN2D_OK;
 }
 
@@ -511,17 +601,25 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   if (rc != SCAN2D_OK) return rc;
   bool xvec, bvec, yvec;
   vec_flags(d, p, x, z, dy, B, C, nullptr, xvec, bvec, yvec);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  // the state-vector outputs take 16-byte stores (tile kernels: dB / dC, warp
+  // kernels: the lane's 4 states); with G > 1 they go to the workspace first
+  // (every workspace region starts at a multiple of 256 bytes from its base)
+  const bool ovec = d.bc_group > 1 ? ((reinterpret_cast<uintptr_t>(w) & 15) == 0)
+                                   : ((reinterpret_cast<uintptr_t>(dB) & 15) == 0 &&
+                                      (reinterpret_cast<uintptr_t>(dC) & 15) == 0);
+  if (!ovec) bvec = false;  // no tile backward (it stores dB / dC with 8 / 16-byte vectors)
   rc = plan_with_flags(d, p, xvec, bvec, false, ptr_align({x, z, B, C, dy, dx, dz, dB, dC}));
   if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
-  unsigned char* w = static_cast<unsigned char*>(ws);
   const ResLayout R = res_layout(d, p);
   const unsigned char* r = static_cast<const unsigned char*>(residual);
   Args<T> a{};
   fill_common(a, d, p, x, z, B, C, A, Dskip, bias);
   set_flags(a, xvec, bvec, yvec);
   a.dy = static_cast<const T*>(dy);
+  a.ovec = ovec;
   a.ckpt = const_cast<T*>(reinterpret_cast<const T*>(r + R.ckpt));
   a.hres = const_cast<T*>(reinterpret_cast<const T*>(r + R.hres));
   a.hcarry = nullptr;
@@ -542,7 +640,8 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   a.dC = dC_ps;
   a.part = reinterpret_cast<T*>(w + L.part);
   a.rcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.rcarry);
-  a.ticket = reinterpret_cast<int*>(w + L.ticket);
+  a.hdr = reinterpret_cast<s2d::WsHdr*>(w + L.ticket);
+  a.ticket = &a.hdr->ticket;
   // per-scan parameters: the kernels finish dA / dbias / dD themselves (fixed
   // strip order, no extra launch); shared parameters need the reduction kernel
   const bool fuse = (p.b.tile || p.b.rows1) && d.params_period == d.num_scans;
@@ -551,11 +650,15 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   a.dA_out = static_cast<T*>(dA);
   a.dbias_out = static_cast<T*>(dbias);
   a.dD_out = static_cast<T*>(dDskip);
-  if (p.b.wreal > 1 &&
-      cudaMemsetAsync(a.ticket, 0, L.cnt + sizeof(int) * static_cast<size_t>(d.num_scans) - L.ticket, stream) !=
-          cudaSuccess)
-    return SCAN2D_ECUDA;
   int launches = 0;
+  if (p.b.wreal > 1) {
+    const size_t cb = L.part - L.rcarry;
+    a.magic = layout_magic(d, p, SCAN2D_OP_BWD, L.rcarry, cb);
+    if (launch_begin(a.hdr, a.magic, d.height, a.scan_cnt, d.num_scans, w + L.rcarry, cb, stream) !=
+        cudaSuccess)
+      return SCAN2D_ECUDA;
+    ++launches;
+  }
   if (s2d::launch_bwd<T>(a, stream) != cudaSuccess) return SCAN2D_ECUDA;
   ++launches;
   if (!fuse) {

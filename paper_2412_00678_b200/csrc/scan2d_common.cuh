@@ -141,11 +141,32 @@ __device__ __forceinline__ void poll_pause() {
 
 // ------------------------------------------------------ gpu-scope carries
 //
-// Tags are unique per (launch, row): the host advances `epoch` by H + 1 per
-// launch, so carry buffers never need clearing between launches; 0 never
-// occurs as a tag (fresh zeroed memory cannot be mistaken for a carry).
+// Workspace header (first bytes of every chained launch's workspace).  The
+// epoch lives in device memory and is advanced by scan2d_begin_kernel, which
+// runs in stream order before every chained launch (so a captured CUDA graph
+// advances it on every replay).  `magic` identifies the workspace layout the
+// carry region was last used with: on a mismatch (fresh memory, or a workspace
+// last used for another descriptor / op) the begin kernel clears the carry
+// region before any tag is trusted; the main kernel then records the magic.
+struct WsHdr {
+  int ticket;      // CTA / warp ticket counter (reset by the begin kernel)
+  uint32_t epoch;  // tag base of the current launch, in [0, kTagSpan)
+  uint32_t magic;  // layout hash of the last launch that used the carry region
+  uint32_t pad;
+};
+//
+// Tags are quiet-NaN bit patterns 0x7fc00001 .. 0x7ffffffd, unique per (launch,
+// row) modulo kTagSpan: no finite float can be mistaken for a tag, and neither
+// can the canonical NaNs 0x7fffffff (GPU) / 0x7fc00000 (CPU) or zeroed memory.
+// Every consumed slot is rewritten by every launch with the same layout, so a
+// stale slot only ever holds the previous launch's tag, and the epoch step
+// (H + 1, or H + 2 when that is a multiple of kTagSpan) makes that tag differ.
+constexpr uint32_t kTagSpan = 0x3ffffdu;
 __device__ __forceinline__ int row_tag(uint32_t epoch, int row) {
-  return static_cast<int>((epoch + static_cast<uint32_t>(row)) % 0x7fffffffu) + 1;
+  return static_cast<int>(0x7fc00001u + (epoch + static_cast<uint32_t>(row)) % kTagSpan);
+}
+__device__ __forceinline__ uint32_t load_epoch(const WsHdr* h) {
+  return *reinterpret_cast<const volatile uint32_t*>(&h->epoch) % kTagSpan;
 }
 //
 // Column-group carries travel between warps (one warp per CTA) through global
@@ -504,9 +525,11 @@ struct Args {
   T* dbias_out;
   T* dD_out;
   CarrySlot<T>* rcarry;  // reverse carry at backward warp boundaries, [S][wreal_b-1][H][N]
-  int* ticket;           // warp ticket counter (zeroed before each chained launch)
-  uint32_t epoch;        // tag base of this launch (see row_tag)
+  int* ticket;           // warp ticket counter (= &hdr->ticket; reset by the begin kernel)
+  WsHdr* hdr;            // workspace header (epoch, layout magic); NULL when nothing is chained
+  uint32_t magic;        // layout hash this launch records in hdr->magic
   int xvec, bvec, yvec;  // 16-byte copy units legal for x-like / B-like spans; vector y stores
+  int ovec;              // backward: dB / dC 16-byte aligned (vector state stores legal)
   // shape
   int64_t S;
   int H, W, N, T_tile, P, G;

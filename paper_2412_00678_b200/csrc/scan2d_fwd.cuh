@@ -83,9 +83,13 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
   const int H = a.H, W = a.W, N = a.N, Np = ge.Np;
 
   int64_t unit = blockIdx.x;
+  const uint32_t epoch = ge.wreal > 1 ? load_epoch(a.hdr) : 0u;
   if (ge.wreal > 1) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1);
+    if (lane == 0) {
+      t = atomicAdd(a.ticket, 1);
+      if (t == 0) a.hdr->magic = a.magic;  // the carry region now follows this layout
+    }
     unit = __shfl_sync(kFull, t, 0);
   }
   const LaneMap lm = lane_map<LPC, J>(ge, unit, lane, a.S, W);
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
         }
         ew[e] = T(0);
       }
-      const int tag = row_tag(a.epoch, i);
+      const int tag = row_tag(epoch, i);
       // ---- carry from the column group on the left
       if (fast_carry) {
         if constexpr (sizeof(T) == 4)

@@ -374,14 +374,19 @@ struct StripId {
   bool valid;
 };
 
-__device__ __forceinline__ StripId strip_id(const Geo& ge, int64_t S, int* ticket, bool rev) {
+template <typename T>
+__device__ __forceinline__ StripId strip_id(const Geo& ge, const Args<T>& a, bool rev) {
   __shared__ int tk;
+  const int64_t S = a.S;
   StripId id;
   id.nw = blockDim.x / 32;
   id.wi = threadIdx.x / 32;
   int64_t unit = blockIdx.x;
   if (ge.wreal > 1) {
-    if (threadIdx.x == 0) tk = atomicAdd(ticket, 1);
+    if (threadIdx.x == 0) {
+      tk = atomicAdd(a.ticket, 1);
+      if (tk == 0) a.hdr->magic = a.magic;  // the carry region now follows this layout
+    }
     __syncthreads();
     unit = tk;
   }
@@ -404,7 +409,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   constexpr uint32_t ES = sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& ge = a.plan.f;
-  const StripId id = strip_id(ge, a.S, a.ticket, false);
+  const StripId id = strip_id(ge, a, false);
+  const uint32_t epoch = ge.wreal > 1 ? load_epoch(a.hdr) : 0u;
   const int lane = threadIdx.x & 31;
   CarryRing<T, SH> ring;
   ring.setup(smem_raw + static_cast<size_t>(id.nw) * TS::F_TOTAL * ES, id.nw);
@@ -520,10 +526,10 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
     } else if (has_pred && row_ok) {
       if constexpr (sizeof(T) == 4) {
         carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
-                          *reinterpret_cast<CarryPre<float, SH>*>(&cpre), row_tag(a.epoch, i1),
+                          *reinterpret_cast<CarryPre<float, SH>*>(&cpre), row_tag(epoch, i1),
                           *reinterpret_cast<float(*)[SH]>(hh));
       } else {
-        carry_get_wait<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
+        carry_get_wait<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(epoch, i1), SH);
       }
     }
     {
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
       // strips other than the last are full (ncols == CW): hh is the boundary carry
       if (succ_ring) ring.put(id.wi, t, lane, hh);
       if (has_succ && row_ok && !succ_ring)
-        carry_put<T, SH>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(a.epoch, i1), SH);
+        carry_put<T, SH>(hc_out + static_cast<size_t>(i1) * N, hh, row_tag(epoch, i1), SH);
       if (save && has_succ && row_ok) stg_stream<T, SH>(hr_out + static_cast<size_t>(i1) * N, hh);
     }
     __syncwarp();
@@ -607,7 +613,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   constexpr uint32_t ES = sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geo& ge = a.plan.b;
-  const StripId id = strip_id(ge, a.S, a.ticket, true);
+  const StripId id = strip_id(ge, a, true);
+  const uint32_t epoch = ge.wreal > 1 ? load_epoch(a.hdr) : 0u;
   const int lane = threadIdx.x & 31;
   CarryRing<T, SH> ring;
   ring.setup(smem_raw + static_cast<size_t>(id.nw) * TS::B_TOTAL * ES, id.nw);
@@ -860,10 +867,10 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
       } else if (has_succ && row_ok) {
         if constexpr (sizeof(T) == 4)
           carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
-                            *reinterpret_cast<CarryPre<float, SH>*>(&rpre), row_tag(a.epoch, i1),
+                            *reinterpret_cast<CarryPre<float, SH>*>(&rpre), row_tag(epoch, i1),
                             *reinterpret_cast<float(*)[SH]>(rho));
         else
-          carry_get_wait<T, SH>(rc_in + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
+          carry_get_wait<T, SH>(rc_in + static_cast<size_t>(i1) * N, rho, row_tag(epoch, i1), SH);
       }
       const T* dr = Ds + r1 * CW;
       const T* ur = DXs + r1 * CW;
@@ -928,7 +935,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
       if (pred_ring)
         ring.put(id.wi, u, lane, rho);
       else if (has_pred && row_ok)
-        carry_put<T, SH>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(a.epoch, i1), SH);
+        carry_put<T, SH>(rc_out + static_cast<size_t>(i1) * N, rho, row_tag(epoch, i1), SH);
     }
     __syncwarp();
     sc = sn;
