@@ -240,9 +240,11 @@ def cpu_reference(wl, target_s=10.0, reps=3, parity_dev=None):
 
 
 def parity_vs_reference(cr, dev, max_scans=16):
-    """North_star parity report: y of the GPU path vs the reference library's
-    fp64 engine on the CPU sample's own inputs (normwise error of
-    test_util.hpp:17-26 and the per-element distribution)."""
+    """North_star parity report on the CPU sample's own inputs: y and (for a
+    training workload) every gradient group of the GPU path against the
+    reference library's fp64 engine (normwise error of test_util.hpp:17-26 and
+    the per-element distribution), with the reference's own fp32 engine on the
+    same inputs beside it for scale."""
     import numpy as np
     import torch
 
@@ -252,20 +254,35 @@ def parity_vs_reference(cr, dev, max_scans=16):
     wl = cr.wl
     k = min(cr.k, max_scans)
     H, W, N = wl["H"], wl["W"], wl["N"]
-    x, z, B, C, A, D, bias, _ = [a[:k] for a in cr.arrs]
-    _, y64 = cr.ref.batch(k, k, 1, H, W, N, 16, cr.threads, False,
-                          *[np.asarray(v, np.float64) for v in (x, z, B, C, A, D, bias)], dtype="f64",
-                          want_y=True)
+    x, z, B, C, A, D, bias, dy = [a[:k] for a in cr.arrs]
+    bwd = wl["bwd"]
     t = [torch.from_numpy(np.ascontiguousarray(v)).to(dev) for v in (x, z, B, C, A, D, bias)]
-    op = Scan2dOp(k, H, W, N, tile=16, device=dev, with_backward=False)
-    y = op.forward(*t, save=False).cpu().numpy()
-    # the reference's own fp32 engine on the same inputs, for scale
-    _, y32 = cr.ref.batch(k, k, 1, H, W, N, 16, cr.threads, False,
-                          *[np.asarray(v, np.float32) for v in (x, z, B, C, A, D, bias)], dtype="f32",
-                          want_y=True)
-    return {"scans": k, "against": "reference tiled_scan_2d_forward<double> (oracle/_ref)",
-            "normwise_rel": rel_error(y, y64), "tolerance": 1e-4, "elem_rel": elem_stats(y, y64),
-            "reference_f32": {"normwise_rel": rel_error(y32, y64), "elem_rel": elem_stats(y32, y64)}}
+    op = Scan2dOp(k, H, W, N, tile=16, device=dev, with_backward=bwd)
+    got = {"y": op.forward(*t, save=bwd).cpu().numpy()}
+    if bwd:
+        g = op.backward(*t, torch.from_numpy(np.ascontiguousarray(dy)).to(dev))
+        for name, v in zip(("dx", "dz", "dA", "dB", "dC", "dD", "dbias"), g):
+            got[name] = v.cpu().numpy()
+    refs = {}
+    for dt in ("f64", "f32"):
+        cast = np.float64 if dt == "f64" else np.float32
+        arrs = [np.asarray(v, cast) for v in (x, z, B, C, A, D, bias, dy)]
+        if bwd:
+            refs[dt] = cr.ref.batch_grads(k, H, W, N, 16, cr.threads, *arrs, dtype=dt)
+        else:
+            _, y_ = cr.ref.batch(k, k, 1, H, W, N, 16, cr.threads, False, *arrs[:7], dtype=dt, want_y=True)
+            refs[dt] = {"y": y_}
+    groups = {}
+    for name, v in got.items():
+        r64 = refs["f64"][name]
+        groups[name] = {"normwise_rel": rel_error(v, r64), "elem_rel": elem_stats(v, r64),
+                        "reference_f32_normwise_rel": rel_error(refs["f32"][name], r64)}
+    worst = max(gv["normwise_rel"] for gv in groups.values())
+    return {"scans": k, "against": "reference tiled_scan_2d_forward/backward<double> (oracle/_ref)",
+            "tolerance": 1e-4, "worst_normwise_rel": worst, "pass": bool(worst <= 1e-4),
+            "normwise_rel": groups["y"]["normwise_rel"], "elem_rel": groups["y"]["elem_rel"],
+            "reference_f32": {"normwise_rel": groups["y"]["reference_f32_normwise_rel"]},
+            "groups": groups}
 
 
 # ----------------------------------------------------------------- main

@@ -23,6 +23,15 @@
  *  - Deterministic: identical inputs give identical output bits run to run (no
  *    floating-point atomics; scalar reductions use a fixed order).
  *  - Thread safe across distinct (stream, workspace) pairs.
+ *  - Workspaces need no initialisation.  Launches whose column strips are
+ *    chained across CTAs keep a small header at the start of the workspace (a
+ *    ticket, a device-side epoch for the carry tags, a layout hash): a short
+ *    begin kernel advances it in stream order, so a call captured in a CUDA
+ *    graph stays correct on every replay.  The first call with a workspace, or
+ *    the first after it served another descriptor / op, clears the workspace's
+ *    carry region once (stale words can never satisfy a tag).
+ *  - Output alignment: none required; 16-byte aligned dB / dC enable the
+ *    vector-store kernels (otherwise a scalar-store kernel family runs).
  *
  * Layouts (S scans = flattened batch x channel, per-scan reference Grid layout,
  * types.hpp:55-57, N fastest):
@@ -193,7 +202,7 @@ int scan2d_forward_variant(const scan2d_desc* desc, int variant, const void* x, 
 int scan2d_plan_info(const scan2d_desc* desc, int op, int64_t* out8);
 
 /* Number of kernel launches the last scan2d_forward / scan2d_backward call on
- * this host thread enqueued (memsets excluded). */
+ * this host thread enqueued (begin kernels included, memsets excluded). */
 int scan2d_last_launch_count(void);
 
 const char* scan2d_status_string(int status);

@@ -113,7 +113,8 @@ int oracle_fwd(int h, int w, int n, const T* x, const T* z, const T* b, const T*
 template <typename T>
 double batch_run(std::int64_t S, int P, int G, int h, int w, int n, int t, int threads,
                  int do_bwd, const T* x, const T* z, const T* b, const T* c, const T* a,
-                 const T* dskip, const T* bias, const T* dy, T* y, T* dx) {
+                 const T* dskip, const T* bias, const T* dy, T* y, T* dx, T* dz = nullptr,
+                 T* da = nullptr, T* db = nullptr, T* dc = nullptr, T* dd = nullptr, T* dbias = nullptr) {
   const std::size_t hw = static_cast<std::size_t>(h) * w, hwn = hw * n;
   if (threads < 1) threads = 1;
   if (threads > S) threads = static_cast<int>(S);
@@ -131,6 +132,13 @@ double batch_run(std::int64_t S, int P, int G, int h, int w, int n, int t, int t
       if (do_bwd) {
         auto gr = tiled_scan_2d_backward(fwd.saved, grid_from(h, w, 1, dy + s * hw));
         if (dx) std::memcpy(dx + s * hw, gr.dx.data.data(), sizeof(T) * hw);
+        // full gradient bundle (per-scan parameters and B/C only: P == S, G == 1)
+        if (dz) std::memcpy(dz + s * hw, gr.dz_raw.data.data(), sizeof(T) * hw);
+        if (da) std::memcpy(da + s * n, gr.da.data(), sizeof(T) * n);
+        if (db) std::memcpy(db + s * hwn, gr.db.data.data(), sizeof(T) * hwn);
+        if (dc) std::memcpy(dc + s * hwn, gr.dc.data.data(), sizeof(T) * hwn);
+        if (dd) dd[s] = gr.dd;
+        if (dbias) dbias[s] = gr.dbias;
       }
     }
   };
@@ -222,6 +230,23 @@ double ref_batch_f64(std::int64_t S, int P, int G, int h, int w, int n, int t, i
                      const double* dy, double* y, double* dx) {
   return batch_run<double>(S, P, G, h, w, n, t, threads, do_bwd, x, z, b, c, a, d, bias, dy, y,
                            dx);
+}
+
+// Every gradient group per scan (P == S, G == 1; the bench's parity report).
+double ref_batch_grads_f32(std::int64_t S, int h, int w, int n, int t, int threads, const float* x,
+                           const float* z, const float* b, const float* c, const float* a,
+                           const float* d, const float* bias, const float* dy, float* y, float* dx,
+                           float* dz, float* da, float* db, float* dc, float* dd, float* dbias) {
+  return batch_run<float>(S, static_cast<int>(S), 1, h, w, n, t, threads, 1, x, z, b, c, a, d, bias, dy, y,
+                          dx, dz, da, db, dc, dd, dbias);
+}
+double ref_batch_grads_f64(std::int64_t S, int h, int w, int n, int t, int threads, const double* x,
+                           const double* z, const double* b, const double* c, const double* a,
+                           const double* d, const double* bias, const double* dy, double* y,
+                           double* dx, double* dz, double* da, double* db, double* dc, double* dd,
+                           double* dbias) {
+  return batch_run<double>(S, static_cast<int>(S), 1, h, w, n, t, threads, 1, x, z, b, c, a, d, bias, dy,
+                           y, dx, dz, da, db, dc, dd, dbias);
 }
 
 }  // extern "C"

@@ -22,11 +22,28 @@ struct Num;
 template <>
 struct Num<float> {
   // exp(x) as 2^(x log2 e) on the MUFU.EX2 pipe; the caller pre-scales A by log2 e
+#ifdef S2D_POLY_EXP  // diagnostics: 2^t by range reduction + degree-7 polynomial (< 1 ulp)
+  static __device__ __forceinline__ float exp_scaled(float t) {
+    t = fmaxf(t, -126.0f);
+    const float k = rintf(t);
+    const float f = t - k;  // exact, |f| <= 0.5
+    float p = 1.5252733804059841e-05f;
+    p = fmaf(p, f, 1.5403530393381608e-04f);
+    p = fmaf(p, f, 1.3333558146428443e-03f);
+    p = fmaf(p, f, 9.6181291076284772e-03f);
+    p = fmaf(p, f, 5.5504108664821580e-02f);
+    p = fmaf(p, f, 2.4022650695910071e-01f);
+    p = fmaf(p, f, 6.9314718055994531e-01f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (static_cast<int>(k) << 23));
+  }
+#else
   static __device__ __forceinline__ float exp_scaled(float x_log2e) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x_log2e));
     return r;
   }
+#endif
   static __device__ __forceinline__ float a_scale(float a) { return a * 1.4426950408889634f; }
   // exp(x) for natural x with the rounding of x log2 e and the low part of
   // log2 e folded back: no per-state systematic bias from a pre-rounded
@@ -46,6 +63,14 @@ struct Num<float> {
   // softplus(v) = max(v, 0) + log1p(exp(-|v|)), log1p(t) = 2 atanh(t / (2 + t)).
   // With s = t/(2+t) in [0, 1/3], the odd atanh series to s^13 leaves a
   // relative error < 2e-8; two MUFU ops (ex2, rcp) and ~14 FMA-pipe ops.
+#ifdef S2D_ACCURATE_SCALARS  // diagnostics: IEEE-accurate scalar functions
+  static __device__ __forceinline__ float softplus(float v) { return v > 20.0f ? v : log1pf(expf(v)); }
+  static __device__ __forceinline__ float sigmoid(float v) {
+    if (v >= 0.0f) return 1.0f / (1.0f + expf(-v));
+    const float e = expf(v);
+    return e / (1.0f + e);
+  }
+#else
   static __device__ __forceinline__ float softplus(float v) {
     const float t = exp_scaled(-fabsf(v) * 1.4426950408889634f);
     const float s = t * rcp(2.0f + t);
@@ -66,6 +91,7 @@ struct Num<float> {
     const float r = rcp(1.0f + e);
     return v >= 0.0f ? r : e * r;
   }
+#endif
 };
 
 template <>

@@ -159,6 +159,9 @@ class RefLib:
             getattr(L, f"ref_oracle_fwd_{suf}").argtypes = [C.c_int] * 3 + [_P] * 5 + [ct, ct] + [_P] * 3
             getattr(L, f"ref_batch_{suf}").argtypes = [C.c_int64] + [C.c_int] * 8 + [_P] * 10
             getattr(L, f"ref_batch_{suf}").restype = C.c_double
+            if hasattr(L, f"ref_batch_grads_{suf}"):
+                getattr(L, f"ref_batch_grads_{suf}").argtypes = [C.c_int64] + [C.c_int] * 5 + [_P] * 16
+                getattr(L, f"ref_batch_grads_{suf}").restype = C.c_double
         L.ref_fill_normal_f64.argtypes = [C.c_uint64, C.c_size_t, _P]
         L.ref_fast_expf.argtypes = [C.c_float]
         L.ref_fast_expf.restype = C.c_float
@@ -237,6 +240,21 @@ class RefLib:
         secs = getattr(self.lib, f"ref_batch_{dtype}")(S, P, G, h, w, n, t, threads, int(do_bwd),
                                                         *[_ptr(v) for v in arrs], _ptr(dyp), _ptr(y), None)
         return secs, y
+
+
+    def batch_grads(self, S, h, w, n, t, threads, x, z, B, Cc, A, D, bias, dy, dtype="f64"):
+        """The reference's tiled forward + backward per scan (P == S, G == 1):
+        y and every gradient group (GradBundle, engine.hpp:71-80)."""
+        dt = _np_dtype(dtype)
+        hw = h * w
+        arrs = [np.ascontiguousarray(v, dt).reshape(-1) for v in (x, z, B, Cc, A, D, bias, dy)]
+        out = dict(y=np.empty(S * hw, dt), dx=np.empty(S * hw, dt), dz=np.empty(S * hw, dt),
+                   dA=np.empty(S * n, dt), dB=np.empty(S * hw * n, dt), dC=np.empty(S * hw * n, dt),
+                   dD=np.empty(S, dt), dbias=np.empty(S, dt))
+        getattr(self.lib, f"ref_batch_grads_{dtype}")(
+            S, h, w, n, t, threads, *[_ptr(v) for v in arrs],
+            *[_ptr(out[k]) for k in ("y", "dx", "dz", "dA", "dB", "dC", "dD", "dbias")])
+        return out
 
 
 def rel_error(got, expect) -> float:

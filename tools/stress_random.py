@@ -6,9 +6,10 @@ fourth case runs on operands shifted one element off 16-byte alignment.
 usage: python tools/stress_random.py <n_cases> [seed] [case,case,... [reps]]
        python tools/stress_random.py big        (a fixed list of large shapes)
 (the optional list re-runs only those case indices, reps times each).
-Prints one line per failure and a summary; exit code 1 if any case fails.  An
-fp32 result over the gate but within 1.5x of the reference's own fp32 error
-(the oracle restates its arithmetic) is reported as a note, not a failure."""
+Prints one line per failure and a summary; exit code 1 if any case fails.  The
+gate is strict (north_star: fp32 normwise <= 1e-4 on y and every gradient
+group); the reference's own fp32 error on a failing case is printed beside it
+for information only."""
 import os
 import sys
 import time
@@ -104,12 +105,8 @@ def main():
                     for k2 in bad:
                         ref32[k2] = (rel_error(y32, ref64y) if k2 == "y" else
                                      rel_error(np.asarray(r32[k2]).reshape(-1), np.asarray(ref[k2]).reshape(-1)))
-                # fp32 scalar sums over large grids can miss 1e-4 in the reference
-                # itself: only a result worse than the reference's own fp32 fails
-                real = {k2: v for k2, v in bad.items() if not (k2 in ref32 and v <= 1.5 * ref32[k2])}
-                tag = "FAIL" if real else "note (within the reference's fp32 error)"
-                fails += 1 if real else 0
-                print(tag, label, {k2: f"{v:.2e}" for k2, v in bad.items()},
+                fails += 1
+                print("FAIL", label, {k2: f"{v:.2e}" for k2, v in bad.items()},
                       "ref-f32:", {k2: f"{v:.2e}" for k2, v in ref32.items()}, flush=True)
         except Exception as exc:  # noqa: BLE001
             fails += 1
