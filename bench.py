@@ -47,6 +47,14 @@ WORKLOADS = {
     "cfg5": dict(S=256, H=1024, W=1024, N=16, bwd=False, desc="giga-pixel: B=1 D=256 N=16 1024x1024 fwd (configs[4])"),
 }
 
+# How `--gpus N` scales each workload (ShardedScan2d: contiguous scan ranges,
+# no collective on the data path).  "weak": the global batch is N x the
+# single-GPU batch (N slides / images -- per-GPU work fixed); "strong": the
+# BASELINE batch itself is split over the N GPUs (configs[3], "batch-sharded
+# over 2/4/8 GPUs").
+SCALING = {"cfg1": "weak", "cfg2": "weak", "cfg5": "weak", "cfg3": "strong", "cfg4a": "strong",
+           "cfg4b": "strong", "cfg4c": "strong", "cfg4d": "strong"}
+
 L2_BYTES = 126 * 1024 * 1024
 NVML_REASONS = {
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -304,14 +312,27 @@ def main():
                     help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), "
                          "vertical carries exchanged point to point, pipelined over scan chunks")
     ap.add_argument("--chunks", type=int, default=8, help="scan chunks of the row-band pipeline")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="weak: global batch = N x the workload's; strong: the workload's batch split over N "
+                         "GPUs (default per workload, see SCALING)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    config = {"workload": args.workload, "desc": wl["desc"], "S_per_gpu": wl["S"], "H": wl["H"], "W": wl["W"],
+    scaling = args.scaling or SCALING[args.workload]
+    S_global = wl["S"] * world if scaling == "weak" else wl["S"]
+    # largest per-GPU shard (launcher.shard_range with quantum 1: per-scan
+    # parameters and B/C), computed here so the reference arm imports nothing
+    # of the package (no repo .so loaded on its path)
+    base, extra = divmod(S_global, world)
+    per_gpu = [base + (1 if r < extra else 0) for r in range(world)]
+    fb0, _ = alg_bytes(dict(wl, S=max(per_gpu)))
+    config = {"workload": args.workload, "desc": wl["desc"], "S_global": S_global, "S_per_gpu": per_gpu, "H": wl["H"], "W": wl["W"],
               "N": wl["N"], "tile": 16, "pass": "fwd+bwd" if wl["bwd"] else "fwd",
-              "parallelism": f"scan-sharded x{world} (no collectives)"}
+              "parallelism": (f"batch-sharded x{world} ({scaling} scaling: contiguous scan ranges per GPU, "
+                              "no collective on the data path)"),
+              "l2": l2_policy(fb0)}
 
     if args.rowband and args.impl == "ours":
         return rowband_main(args, wl, rank, world, local, config)
@@ -327,7 +348,7 @@ def main():
         value = cr.gelem_s(mean_s)
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": args.dtype,
                 "data": "synthetic (random_instance distribution)", "config": config,
                 "cpu_baseline": dict(cr.describe(mean_s, args.steps), value=value),
                 "e2e": {"value": value, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -341,9 +362,16 @@ def main():
     dev = torch.device("cuda", local)
     from paper_2412_00678_b200.api import Scan2dOp
 
+    from paper_2412_00678_b200.launcher import ShardedScan2d
+
     dtype = torch.float32
-    ins, dy = synth_inputs(torch, wl, dev, 1234 + rank, dtype)
-    op = Scan2dOp(wl["S"], wl["H"], wl["W"], wl["N"], tile=16, dtype=dtype, device=dev, with_backward=wl["bwd"])
+    sharded = ShardedScan2d(S_global, wl["H"], wl["W"], wl["N"], rank, world, dist=dist, tile=16, dtype=dtype,
+                            device=dev, with_backward=wl["bwd"])
+    shard = sharded.shard
+    wl_local = dict(wl, S=shard.count)  # this rank's contiguous scan range of the global batch
+    assert [sh.count for sh in sharded.shards] == per_gpu
+    ins, dy = synth_inputs(torch, wl_local, dev, 1234 + shard.s0, dtype)
+    op = sharded.op
 
     def step():
         op.forward(*ins, save=wl["bwd"])
@@ -371,7 +399,7 @@ def main():
     t_host0 = time.perf_counter()
     # inputs smaller than 2x L2: flush L2 between timed steps (a 512 MB write,
     # outside the per-step events) and time the steps by their own events
-    fb0, _ = alg_bytes(wl)
+    fb0, _ = alg_bytes(wl_local)
     flush = fb0 < 2 * L2_BYTES
     scratch = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev) if flush else None
     e_start.record(stream)
@@ -391,9 +419,6 @@ def main():
     barrier()
     launches = op.launches
     total_ms = (sum(a.elapsed_time(c) for a, _, c in evs) if flush else e_start.elapsed_time(e_end))
-    config["l2"] = ("inputs {:.0f} MB < 2x L2: L2 flushed (512 MB write) between timed steps, steps timed by "
-                    "their own events".format(fb0 / 1e6) if flush else
-                    "inputs {:.0f} MB > 2x L2 (2 x 126 MB): no flush needed".format(fb0 / 1e6))
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in evs)
     bwd_ms = statistics.mean(b.elapsed_time(c) for _, b, c in evs) if wl["bwd"] else 0.0
     if dist is not None:
@@ -401,10 +426,10 @@ def main():
     sampler.stop()
     clocks = sampler.summary(t_host0, t_host1)
     ms_per_step = total_ms / args.steps
-    elems = wl["S"] * wl["H"] * wl["W"] * world
+    elems = S_global * wl["H"] * wl["W"]  # the whole job: every rank's scans
     value = elems / (ms_per_step * 1e-3) / 1e9
 
-    fb, bb = alg_bytes(wl)
+    fb, bb = alg_bytes(wl_local)  # the dominant kernel's launch on one GPU
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.workload)
     # kernel family the library picks (scan2d_capi.cu: rows1_shape, use_tile_*)
@@ -422,7 +447,8 @@ def main():
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src, "frac_of_nominal_8000": achieved / 8000.0,
-            "traffic": traffic.get(dom_name, {}).get("dram_bytes_per_launch"),
+            "traffic": (None if traffic.get(dom_name, {}).get("dram_bytes_per_launch") is None else
+                        traffic[dom_name]["dram_bytes_per_launch"] * shard.count / wl["S"]),
             "algorithmic_bytes_per_launch": dom_bytes,
             "launch_ms": dom_ms}
     extra = {"fwd_ms": fwd_ms, "fwd_gbs": fb / (fwd_ms * 1e-3) / 1e9, "fwd_frac": fb / (fwd_ms * 1e-3) / 1e9 / peak}
@@ -474,7 +500,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (random_instance distribution, generated on device)",
                 "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, **extra}
@@ -482,6 +508,15 @@ def main():
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def l2_policy(fwd_bytes):
+    """How the timed loop keeps L2 from serving repeated inputs (the same
+    string in both arms' config)."""
+    if fwd_bytes < 2 * L2_BYTES:
+        return ("inputs {:.0f} MB < 2x L2: L2 flushed (512 MB write) between timed steps, steps timed by their "
+                "own events".format(fwd_bytes / 1e6))
+    return "inputs {:.0f} MB > 2x L2 (2 x 126 MB): no flush needed".format(fwd_bytes / 1e6)
 
 
 def init_dist(torch, world, local):

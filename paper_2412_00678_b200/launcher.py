@@ -67,6 +67,90 @@ def shard_views(shard: Shard, x, z, B, C, A, Dskip, bias, params_period: int, bc
     return x[s0:s1], z[s0:s1], B[g0:g1], C[g0:g1], A, Dskip, bias
 
 
+class ShardedScan2d:
+    """Batch shard of ONE global problem (S scans, H x W, N states, parameter
+    period P, B/C group G) over `world` ranks, one GPU each (SURVEY.md §8e;
+    BASELINE configs[3] "batch-sharded over 2/4/8 GPUs").
+
+    Rank r owns the contiguous, layout-quantum-aligned scan range
+    ``shard_range(S, world, r, layout_quantum(S, P, G))`` and runs the
+    single-GPU operator on it (``op_factory(S_local, P_local, G)``, by default
+    a preallocated ``Scan2dOp``).  The data path has no collective: scans are
+    independent.  Off the timed path, ``gather`` assembles per-scan outputs on
+    every rank (all_gather of equal-sized padded blocks) and
+    ``reduce_shared_params`` sums the per-rank partial gradients of shared
+    parameter rows (P < S) in rank order (deterministic)."""
+
+    def __init__(self, S, H, W, N, rank, world, params_period=None, bc_group=1, op_factory=None, dist=None,
+                 **op_kwargs):
+        self.S, self.H, self.W, self.N = S, H, W, N
+        self.P = S if params_period is None else params_period
+        self.G = bc_group
+        self.rank, self.world, self.dist = rank, world, dist
+        self.quantum = layout_quantum(S, self.P, self.G)
+        self.shard = shard_range(S, world, rank, self.quantum)
+        self.shards = [shard_range(S, world, r, self.quantum) for r in range(world)]
+        self.per_scan_params = self.P == S
+        self.P_local = self.shard.count if self.per_scan_params else self.P
+        if op_factory is None:
+            from .api import Scan2dOp
+
+            def op_factory(s_loc, p_loc, g):
+                return Scan2dOp(s_loc, H, W, N, params_period=p_loc, bc_group=g, **op_kwargs)
+        self.op = op_factory(self.shard.count, self.P_local, self.G) if self.shard.count > 0 else None
+
+    def views(self, x, z, B, C, A, Dskip, bias):
+        """This rank's slices of the global operands (C-ABI layouts)."""
+        return shard_views(self.shard, x, z, B, C, A, Dskip, bias, self.P, self.G)
+
+    def forward(self, *shard_ins, **kw):
+        if self.op is None:  # empty shard (fewer layout quanta than ranks)
+            return shard_ins[0].new_empty((0, self.H, self.W))
+        return self.op.forward(*shard_ins, **kw)
+
+    def backward(self, *shard_ins_and_dy):
+        if self.op is None:
+            x, A = shard_ins_and_dy[0], shard_ins_and_dy[4]
+            e = lambda *s: x.new_zeros(s)  # noqa: E731
+            p = 0 if self.per_scan_params else self.P
+            H, W, N = self.H, self.W, self.N
+            return e(0, H, W), e(0, H, W), A.new_zeros((p, N)), e(0, H, W, N), e(0, H, W, N), e(p), e(p)
+        return self.op.backward(*shard_ins_and_dy)
+
+    def gather(self, t, scans_per_row=1):
+        """All-gather a per-scan output (leading dim = this rank's scans //
+        scans_per_row, e.g. G for dB / dC) into the global tensor on every rank."""
+        import torch
+
+        counts = [sh.count // scans_per_row for sh in self.shards]
+        if self.world == 1 or self.dist is None:
+            return t
+        m = max(counts)
+        pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        bufs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(bufs, pad)
+        return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+
+    def gather_grads(self, grads):
+        """(dx, dz, dA, dB, dC, dD, dbias) of this shard -> the global bundle:
+        per-scan groups concatenated in scan order; shared parameter rows
+        (P < S) summed over ranks in rank order."""
+        dx, dz, dA, dB, dC, dD, dbias = grads
+        out = [self.gather(dx), self.gather(dz)]
+        if self.per_scan_params:
+            pA, pD, pb = self.gather(dA), self.gather(dD), self.gather(dbias)
+        else:
+            pA, pD, pb = self.reduce_shared_params([dA, dD, dbias])
+        out += [pA, self.gather(dB, self.G), self.gather(dC, self.G), pD, pb]
+        return out
+
+    def reduce_shared_params(self, parts):
+        if self.world == 1 or self.dist is None:
+            return parts
+        return reduce_params(self.dist, parts, self.world)
+
+
 # ---------------------------------------------------------------- row bands
 #
 # Optional row-band shard of ONE giant scan (SURVEY.md §8e, config 5): rank r
