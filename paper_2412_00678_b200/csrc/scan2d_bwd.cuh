@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_bwd_kernel(const Args<T> a) {
   const int K = a.plan.K, nb = a.plan.nb;
 
   int64_t unit = blockIdx.x;
+  if (ge.wreal > 1) griddep_wait();  // the begin kernel's header writes are visible
   const uint32_t epoch = ge.wreal > 1 ? load_epoch(a.hdr) : 0u;
   if (ge.wreal > 1) {
     int t = 0;

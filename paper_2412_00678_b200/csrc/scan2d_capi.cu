@@ -162,6 +162,11 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p.b = make_geo(d, true);
   p.f = make_geo(d, false);
   p.pfd = env_int("SCAN2D_ROWS1_PFD", 6);  // measured: 6 rows ahead best on cfg3 / cfg4a (4..12, 1000 = off)
+  // tile kernels: bulk L2 prefetch distance in tiles (1000 = off)
+  p.pft_f = env_int("SCAN2D_TILE_PFF", 1000);
+  p.pft_b = env_int("SCAN2D_TILE_PFB", 1);  // measured on cfg2: 1 tile ahead 0.308 vs 0.326 ms
+  if (p.pft_f >= 1000) p.pft_f = 0;
+  if (p.pft_b >= 1000) p.pft_b = 0;
   if (rows1_shape(d)) {
     p.K = 4;
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
@@ -408,6 +413,7 @@ __global__ void scan2d_begin_kernel(s2d::WsHdr* h, uint32_t magic, uint32_t step
   for (int64_t i = tid; i < ncnt; i += nth) cnt[i] = 0;
   if (fresh)
     for (int64_t i = tid; i < nclr; i += nth) clr[i] = make_uint4(0u, 0u, 0u, 0u);
+  s2d::griddep_launch_dependents();  // the chained kernel may launch now; it waits for our writes
   if (tid == 0) {
     h->ticket = 0;
     h->epoch = fresh ? 0u : (h->epoch % s2d::kTagSpan + step) % s2d::kTagSpan;
@@ -570,6 +576,7 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
     a.magic = layout_magic(d, p, SCAN2D_OP_FWD, L.hcarry, cb);
     if (launch_begin(a.hdr, a.magic, d.height, nullptr, 0, w + L.hcarry, cb, stream) != cudaSuccess)
       return SCAN2D_ECUDA;
+    a.pdl = env_int("SCAN2D_PDL", 1) == 1;
     ++launches;
   }
   if (ph != nullptr) {
@@ -657,6 +664,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
     if (launch_begin(a.hdr, a.magic, d.height, a.scan_cnt, d.num_scans, w + L.rcarry, cb, stream) !=
         cudaSuccess)
       return SCAN2D_ECUDA;
+    a.pdl = env_int("SCAN2D_PDL", 1) == 1;
     ++launches;
   }
   if (s2d::launch_bwd<T>(a, stream) != cudaSuccess) return SCAN2D_ECUDA;

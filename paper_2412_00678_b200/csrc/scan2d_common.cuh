@@ -188,8 +188,22 @@ struct WsHdr {
 // stale slot only ever holds the previous launch's tag, and the epoch step
 // (H + 1, or H + 2 when that is a multiple of kTagSpan) makes that tag differ.
 constexpr uint32_t kTagSpan = 0x3ffffdu;
+#ifdef S2D_MASK_TAG
+__device__ __forceinline__ int row_tag(uint32_t epoch, int row) {
+  return static_cast<int>(0x7fc00001u + ((epoch + static_cast<uint32_t>(row)) & 0x1fffffu));
+}
+#else
 __device__ __forceinline__ int row_tag(uint32_t epoch, int row) {
   return static_cast<int>(0x7fc00001u + (epoch + static_cast<uint32_t>(row)) % kTagSpan);
+}
+#endif
+// Programmatic dependent launch: a chained kernel is launched while its begin
+// kernel may still run; it waits here (before touching the header or any
+// carry slot) until the begin kernel's writes are visible.  A no-op when the
+// kernel was launched without the PDL attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t load_epoch(const WsHdr* h) {
   return *reinterpret_cast<const volatile uint32_t*>(&h->epoch) % kTagSpan;
@@ -512,6 +526,7 @@ struct Plan {
   int nq;     // ceil(W / Q) - 1 carry boundaries per row
   int warp_ok;  // the warp kernels' geometry fits this residual layout (else tile / rows1 kernels only)
   int pfd;      // N = 1 forward: L2 prefetch distance in rows
+  int pft_f, pft_b;  // tile kernels: bulk L2 prefetch distance in tiles (forward / backward; 0 = off)
 };
 
 template <typename T>
@@ -554,6 +569,7 @@ struct Args {
   int* ticket;           // warp ticket counter (= &hdr->ticket; reset by the begin kernel)
   WsHdr* hdr;            // workspace header (epoch, layout magic); NULL when nothing is chained
   uint32_t magic;        // layout hash this launch records in hdr->magic
+  int pdl;               // launch with programmatic stream serialization (after a begin kernel)
   int xvec, bvec, yvec;  // 16-byte copy units legal for x-like / B-like spans; vector y stores
   int ovec;              // backward: dB / dC 16-byte aligned (vector state stores legal)
   // shape

@@ -289,6 +289,35 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// Bulk L2 prefetch by the TMA unit (UBLKPF): `bytes` (multiple of 16) from a
+// 16-byte aligned address, no registers, no completion tracking.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Rows r0 .. r0+R-1 of the strip, one row per lane: the B / C spans (ncols x N
+// elements each) and the per-cell planes (x, z and, backward, dy) prefetched
+// into L2 by the TMA unit, so the tile's register / cp.async loads hit L2.
+template <typename T, int R>
+__device__ __forceinline__ void prefetch_tile_l2(int lane, int r0, int H, int ncols, int N, size_t WN, int W,
+                                                 const T* Bs, const T* Cs, const T* xs, const T* zs,
+                                                 const T* ys) {
+  const int planes = ys != nullptr ? 5 : 4;
+  if (lane < planes * R) {
+    const int r = r0 + lane % R, k = lane / R;
+    if (r < H) {
+      const uint32_t sb = static_cast<uint32_t>(ncols * N * sizeof(T));
+      const uint32_t sx = static_cast<uint32_t>(ncols * sizeof(T));
+      const T* p = k == 0 ? Bs + static_cast<size_t>(r) * WN
+                 : k == 1 ? Cs + static_cast<size_t>(r) * WN
+                 : k == 2 ? xs + static_cast<size_t>(r) * W
+                 : k == 3 ? zs + static_cast<size_t>(r) * W
+                          : ys + static_cast<size_t>(r) * W;
+      bulk_prefetch_l2(p, k < 2 ? sb : sx);
+    }
+  }
+}
+
 
 // ------------------------------------------------------------ CTA = strips
 //
@@ -383,6 +412,7 @@ __device__ __forceinline__ StripId strip_id(const Geo& ge, const Args<T>& a, boo
   id.wi = threadIdx.x / 32;
   int64_t unit = blockIdx.x;
   if (ge.wreal > 1) {
+    griddep_wait();  // the begin kernel has reset the ticket and advanced the epoch
     if (threadIdx.x == 0) {
       tk = atomicAdd(a.ticket, 1);
       if (tk == 0) a.hdr->magic = a.magic;  // the carry region now follows this layout
@@ -476,10 +506,15 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   T bc[CW][SH];
   load_b_rows<T, CW, SH>(bc, Bg, r1, H, WN, ncols, N);
 
+  const int pft = a.plan.pft_f;
   for (int t = 0; t < ntiles; ++t) {
     const int r0 = t * R;
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
+#ifndef S2D_NO_PF
+    if (pft > 0 && t + pft < ntiles)
+      prefetch_tile_l2<T, R>(lane, r0 + pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr);
+#endif
     // ---- prefetch tile t+1: C into the free slot, x / z into the other parity
     //      (its B operand is loaded into the same registers right after phase 1)
     if (t + 1 < ntiles) {
@@ -707,9 +742,14 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     if (has_pred && ib < H) ldg_states<T, SH>(hh0n, hc_in + static_cast<size_t>(ib) * N);
   }
 
+  const int pft = a.plan.pft_b;
   for (int t = ntiles - 1; t >= 0; --t) {
     const int u = ntiles - 1 - t;  // visiting index (ring phase)
     const int r0 = t * R;
+#ifndef S2D_NO_PF
+    if (pft > 0 && t - pft >= 0)
+      prefetch_tile_l2<T, R>(lane, r0 - pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg);
+#endif
     const int rows = min(R, H - r0);
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
