@@ -312,10 +312,14 @@ def main():
                     help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), "
                          "vertical carries exchanged point to point, pipelined over scan chunks")
     ap.add_argument("--chunks", type=int, default=8, help="scan chunks of the row-band pipeline")
+    ap.add_argument("--compare", action="store_true",
+                    help="Table 3: tiled vs naive-2D vs flat-1D operators at 14^2/56^2/200^2, D=1 N=16")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="weak: global batch = N x the workload's; strong: the workload's batch split over N "
                          "GPUs (default per workload, see SCALING)")
     args = ap.parse_args()
+    if args.compare:
+        return compare_main(args)
     wl = dict(WORKLOADS[args.workload])
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -507,6 +511,85 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    return 0
+
+
+# Table 3 of the paper: CUDA operators, one feature map per
+# call (D = 1), N = 16, throughput in feature maps per second.
+PAPER_TABLE3 = {"cub_1d": {14: 49e3, 56: 12e3, 200: 3e3}, "naive_2d": {14: 0.2e3, 56: 0.06e3, 200: 0.02e3},
+                "tiled_2d": {14: 40e3, 56: 6e3, 200: 1e3}}
+
+
+def compare_main(args):
+    """Table 3 on B200: the tiled operator against the two comparators behind
+    the same C ABI (naive 2D: N horizontal state maps in HBM, engine.cpp:412-487;
+    flat 1D: block scan of the row-major flattening, engine.cpp:489-526), D = 1,
+    N = 16, at 14^2 / 56^2 / 200^2.  Each call is one forward on S maps; K calls
+    are captured in a CUDA graph and replayed, so the time is the device's (no
+    Python launch overhead).  maps/s = S * K / time.  S = 1 is the paper's
+    "single dimensional feature input"; S = 128 the batched throughput."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2412_00678_b200 import _native as nat
+    from paper_2412_00678_b200.api import Scan2dOp
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    rows = []
+    K = 20
+    for hw in (14, 56, 200):
+        for S in (1, 128):
+            wl = dict(S=S, H=hw, W=hw, N=16)
+            ins, _ = synth_inputs(torch, wl, dev, 77, torch.float32)
+            y = torch.empty(S, hw, hw, device=dev)
+            desc = nat.make_desc(S, hw, hw, 16)
+            op = Scan2dOp(S, hw, hw, 16, device=dev, with_backward=False)
+            op.check = False
+            ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+            calls = {"tiled_2d": lambda: op.forward(*ins, save=False)}
+            for name, var in (("naive_2d", nat.VARIANT_NAIVE), ("cub_1d", nat.VARIANT_FLAT1D)):
+                wsb = nat.lib.scan2d_comparator_workspace_bytes(C.byref(desc), var)
+                ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+
+                def call(var=var, ws=ws, wsb=wsb):
+                    rc = nat.lib.scan2d_forward_variant(
+                        C.byref(desc), var, *[ptr(t) for t in ins], ptr(y), ptr(ws), wsb,
+                        C.c_void_p(torch.cuda.current_stream().cuda_stream))
+                    if rc != nat.OK:
+                        raise RuntimeError(f"scan2d_forward_variant: {nat.status_string(rc)}")
+                calls[name] = call
+            for name, fn in calls.items():
+                if name == "naive_2d" and hw == 200 and S == 128:
+                    continue  # 26 GB of state maps: beyond the point of the comparison
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(side):
+                    for _ in range(3):
+                        fn()
+                torch.cuda.current_stream(dev).wait_stream(side)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for _ in range(K):
+                        fn()
+                g.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 5
+                e0.record()
+                for _ in range(reps):
+                    g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / (reps * K)
+                rows.append({"variant": name, "hw": hw, "maps_per_call": S, "us_per_call": ms * 1e3,
+                             "maps_per_s": S / (ms * 1e-3),
+                             "paper_maps_per_s": PAPER_TABLE3[name][hw] if S == 1 else None})
+    print(json.dumps({"compare": "Table 3 (PAPER.md:280-282) on one B200: D=1 N=16 fp32 forward, CUDA-graph "
+                                 "replay of 20 calls (device time), inputs L2-resident like the paper's repeated "
+                                 "inference calls", "rows": rows}), flush=True)
     return 0
 
 

@@ -167,6 +167,17 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p.pft_b = env_int("SCAN2D_TILE_PFB", 1);  // measured on cfg2: 1 tile ahead 0.308 vs 0.326 ms
   if (p.pft_f >= 1000) p.pft_f = 0;
   if (p.pft_b >= 1000) p.pft_b = 0;
+  // small problems (inputs well inside L2): the tile kernels prefetch every
+  // tile of their strip into L2 at the start, so only the first tile waits on
+  // DRAM (latency-bound launches: cfg1, Table 3's single maps)
+  {
+    const size_t es = dtype_size(d.dtype);
+    const size_t in_bytes = es * static_cast<size_t>(d.num_scans) * d.height * d.width * (3 + 2 * d.state_dim);
+    // (few tiles only: every row of every plane is one bulk prefetch, and a
+    // long queue of them measured slower -- 56^2 / 200^2 single maps)
+    p.pf_all = in_bytes <= (static_cast<size_t>(env_int("SCAN2D_PF_ALL_MB", 48)) << 20) &&
+               d.height <= env_int("SCAN2D_PF_ALL_ROWS", 32);
+  }
   if (rows1_shape(d)) {
     p.K = 4;
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
@@ -237,14 +248,16 @@ void vec_flags(const scan2d_desc& d, const Plan& p, const void* x, const void* z
   yvec = al(y) && (d.width % 4) == 0;
 }
 
-// Tile-transpose forward (scan2d_tile.cuh): N in {4, 8, 16, 32}, 16-byte copy
-// units legal, strips of 16 columns (the carry grid Q becomes 16).
+// Tile-transpose kernels (scan2d_tile2.cuh): N in {4, 8, 16, 32}, 16-byte
+// aligned B / C rows, strips of 16 columns (the carry grid Q becomes 16); x / z
+// / dy rows that are not 16-byte aligned are staged element by element.
 // (Reference CarryState emission -- ph / pv, only the C++ shim asks for it --
 // runs on the warp kernel instead: the residual layout is the same.)
 bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec, bool emit) {
+  (void)xvec;  // x / z / dy rows that are not 16-byte aligned take element copies (issue_cells)
   if (emit) return false;
   const int N = d.state_dim;
-  if (!(N == 4 || N == 8 || N == 16 || N == 32) || !xvec || !bvec) return false;
+  if (!(N == 4 || N == 8 || N == 16 || N == 32) || !bvec) return false;
   return env_int("SCAN2D_TILE_FWD", 1) == 1;
 }
 

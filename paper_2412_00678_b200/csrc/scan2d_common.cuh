@@ -159,11 +159,15 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 // far longer than asked on sm_100 when the word is not ready yet (one global
 // hop between two CTAs measured 2.2x slower with it); a short clock spin keeps
 // the re-poll latency near the L2 round trip.
+#ifdef S2D_NO_POLL_PAUSE
+__device__ __forceinline__ void poll_pause() {}
+#else
 __device__ __forceinline__ void poll_pause() {
   const long long t0 = clock64();
   while (clock64() - t0 < 64) {
   }
 }
+#endif
 
 // ------------------------------------------------------ gpu-scope carries
 //
@@ -527,6 +531,7 @@ struct Plan {
   int warp_ok;  // the warp kernels' geometry fits this residual layout (else tile / rows1 kernels only)
   int pfd;      // N = 1 forward: L2 prefetch distance in rows
   int pft_f, pft_b;  // tile kernels: bulk L2 prefetch distance in tiles (forward / backward; 0 = off)
+  int pf_all;        // tile kernels: prefetch the whole strip into L2 at the start (small problems)
 };
 
 template <typename T>

@@ -121,6 +121,129 @@ __global__ void flat_readout_kernel(const T* __restrict__ x, const T* __restrict
   y[t] = fma(Dskip[p], x[t], acc);
 }
 
+// flat1d, parallel (the "CUB 1D scan" of Table 3 / Mamba's selective scan;
+// block_scan_1d_forward's segmented block scan, block_scan.cpp:28-88, on the
+// GPU): one CTA per scan walks the row-major flattened grid in chunks of
+// kThreads x kEpt elements.  Per chunk and state d: the affine pairs
+// (Abar, Bbar x) of a thread's kEpt elements are folded in registers, the
+// kThreads folds are combined by a warp shuffle scan and a scan over the warp
+// totals in shared memory, the running carry of the previous chunks enters as
+// the head of the sequence (b <- fma(a, carry, b), block_scan.cpp:51), and
+// y accumulates C_d h over d ascending in registers (engine.cpp:506-518) --
+// the N state sequences never touch HBM.  B and C of the chunk are staged in
+// shared memory with coalesced loads.
+constexpr int kFlatThreads = 256;
+constexpr int kFlatEpt = 2;
+constexpr int kFlatMaxN = 16;  // larger N: the sequential flat kernels above
+
+template <typename T, int N>
+__global__ void __launch_bounds__(kFlatThreads) flat_block_kernel(
+    const T* __restrict__ x, const T* __restrict__ z, const T* __restrict__ B, const T* __restrict__ C,
+    const T* __restrict__ A, const T* __restrict__ Dskip, const T* __restrict__ bias, int64_t L, int P, int G,
+    T* __restrict__ y) {
+  constexpr int CH = kFlatThreads * kFlatEpt;
+  constexpr int NW = kFlatThreads / 32;
+  extern __shared__ __align__(16) unsigned char flat_smem[];
+  T* sB = reinterpret_cast<T*>(flat_smem);          // [CH][N]
+  T* sC = sB + CH * N;                              // [CH][N]
+  T* wa = sC + CH * N;                              // [NW][N] warp totals (a)
+  T* wb = wa + NW * kFlatMaxN;                      // [NW][N] warp totals (b)
+  T* carry = wb + NW * kFlatMaxN;                   // [N] running h
+  const int64_t s = blockIdx.x;
+  const int64_t p = s % P, g = s / G;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const T bs = bias[p], dsk = Dskip[p];
+  for (int d = tid; d < N; d += kFlatThreads) carry[d] = T(0);
+  const T* xs = x + s * L;
+  const T* zs = z + s * L;
+  const T* Bs = B + g * L * N;
+  const T* Cs = C + g * L * N;
+  for (int64_t base = 0; base < L; base += CH) {
+    const int cnt = static_cast<int>(L - base < CH ? L - base : CH);
+    __syncthreads();  // previous chunk done with sB / sC / carry reads
+    for (int e = tid; e < cnt * N; e += kFlatThreads) {
+      sB[e] = Bs[base * N + e];
+      sC[e] = Cs[base * N + e];
+    }
+    T dl[kFlatEpt], xv[kFlatEpt], yacc[kFlatEpt];
+#pragma unroll
+    for (int k = 0; k < kFlatEpt; ++k) {
+      const int idx = tid * kFlatEpt + k;
+      const bool ok = idx < cnt;
+      xv[k] = ok ? xs[base + idx] : T(0);
+      dl[k] = ok ? Num<T>::softplus(zs[base + idx] + bs) : T(0);
+      yacc[k] = T(0);
+    }
+    __syncthreads();
+    T fa[N], fb[N];  // this thread's exclusive prefix within its warp
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      const T ad = Num<T>::a_scale(A[p * N + d]);
+      T aa = T(1), bb = T(0);
+#pragma unroll
+      for (int k = 0; k < kFlatEpt; ++k) {
+        const int idx = tid * kFlatEpt + k;
+        const bool ok = idx < cnt;
+        const T av = ok ? Num<T>::exp_scaled(dl[k] * ad) : T(1);
+        const T bx = ok ? (dl[k] * sB[idx * N + d]) * xv[k] : T(0);
+        bb = fma(av, bb, bx);
+        aa = av * aa;
+      }
+      // inclusive warp scan of the folds (compose: earlier first)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T pa = __shfl_up_sync(kFull, aa, o), pb = __shfl_up_sync(kFull, bb, o);
+        if (lane >= o) {
+          bb = fma(aa, pb, bb);
+          aa = aa * pa;
+        }
+      }
+      if (lane == 31) {
+        wa[wid * kFlatMaxN + d] = aa;
+        wb[wid * kFlatMaxN + d] = bb;
+      }
+      // exclusive within the warp
+      const T ea = __shfl_up_sync(kFull, aa, 1), eb = __shfl_up_sync(kFull, bb, 1);
+      fa[d] = lane == 0 ? T(1) : ea;
+      fb[d] = lane == 0 ? T(0) : eb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      // prefix = carry, then the totals of the warps before this one, then the lane prefix
+      T h = carry[d];
+      for (int w = 0; w < wid; ++w) h = fma(wa[w * kFlatMaxN + d], h, wb[w * kFlatMaxN + d]);
+      h = fma(fa[d], h, fb[d]);
+      const T ad = Num<T>::a_scale(A[p * N + d]);
+#pragma unroll
+      for (int k = 0; k < kFlatEpt; ++k) {
+        const int idx = tid * kFlatEpt + k;
+        if (idx < cnt) {
+          const T av = Num<T>::exp_scaled(dl[k] * ad);
+          h = fma(av, h, (dl[k] * sB[idx * N + d]) * xv[k]);
+          yacc[k] = fma(sC[idx * N + d], h, yacc[k]);
+        }
+      }
+      if (tid * kFlatEpt + kFlatEpt - 1 >= cnt - 1 && tid * kFlatEpt <= cnt - 1) fb[d] = h;  // chunk's last h
+    }
+#pragma unroll
+    for (int k = 0; k < kFlatEpt; ++k) {
+      const int idx = tid * kFlatEpt + k;
+      if (idx < cnt) y[s * L + base + idx] = fma(dsk, xv[k], yacc[k]);
+    }
+    __syncthreads();  // every thread has read carry[]
+    if (tid * kFlatEpt + kFlatEpt - 1 >= cnt - 1 && tid * kFlatEpt <= cnt - 1) {
+#pragma unroll
+      for (int d = 0; d < N; ++d) carry[d] = fb[d];
+    }
+  }
+}
+
+size_t flat_block_smem(int N, size_t es) {
+  return es * (2 * static_cast<size_t>(kFlatThreads) * kFlatEpt * N + 2 * (kFlatThreads / 32) * kFlatMaxN +
+               kFlatMaxN);
+}
+
 unsigned blocks_for(int64_t n, int threads) { return static_cast<unsigned>((n + threads - 1) / threads); }
 
 template <typename T>
@@ -146,6 +269,30 @@ int run_flat(const scan2d_desc& d, const void* x, const void* z, const void* B, 
              const void* Dskip, const void* bias, void* y, void* ws, cudaStream_t st) {
   const int64_t S = d.num_scans;
   const int64_t L = static_cast<int64_t>(d.height) * d.width;
+  if (d.state_dim <= kFlatMaxN && (d.state_dim & (d.state_dim - 1)) == 0) {
+    const size_t smem = flat_block_smem(d.state_dim, sizeof(T));
+    const unsigned grid = static_cast<unsigned>(S);
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kern) {
+      if (smem > 48 * 1024)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e == cudaSuccess)
+        kern<<<grid, kFlatThreads, smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(z),
+                                               static_cast<const T*>(B), static_cast<const T*>(C),
+                                               static_cast<const T*>(A), static_cast<const T*>(Dskip),
+                                               static_cast<const T*>(bias), L, d.params_period, d.bc_group,
+                                               static_cast<T*>(y));
+    };
+    switch (d.state_dim) {
+      case 1: go(flat_block_kernel<T, 1>); break;
+      case 2: go(flat_block_kernel<T, 2>); break;
+      case 4: go(flat_block_kernel<T, 4>); break;
+      case 8: go(flat_block_kernel<T, 8>); break;
+      default: go(flat_block_kernel<T, 16>); break;
+    }
+    if (e != cudaSuccess) return SCAN2D_ECUDA;
+    return cudaGetLastError() == cudaSuccess ? SCAN2D_OK : SCAN2D_ECUDA;
+  }
   T* hs = static_cast<T*>(ws);
   const int th = 128;
   flat_scan_kernel<T><<<blocks_for(S * d.state_dim, th), th, 0, st>>>(
@@ -175,6 +322,8 @@ size_t scan2d_comparator_workspace_bytes(const scan2d_desc* d, int variant) {
   const size_t es = d->dtype == SCAN2D_F64 ? 8 : 4;
   const size_t S = static_cast<size_t>(d->num_scans), HW = static_cast<size_t>(d->height) * d->width;
   if (variant == SCAN2D_VARIANT_NAIVE) return es * S * d->state_dim * (HW + d->width);
+  if (d->state_dim <= s2d::kFlatMaxN && (d->state_dim & (d->state_dim - 1)) == 0)
+    return 16;  // block-scan kernel: no HBM state sequences
   return es * S * HW * d->state_dim;
 }
 

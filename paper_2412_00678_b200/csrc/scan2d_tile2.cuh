@@ -228,9 +228,21 @@ __device__ __forceinline__ ColVec<T, SV> col_vec(int j2) {
 // by the strip's first column) -> [R][CW] in shared memory, 16-byte units
 template <typename TS, typename T>
 __device__ __forceinline__ void issue_cells(uint32_t sdst, const T* g, int r0, int H, int W, int ncols,
-                                            int lane) {
+                                            int lane, bool vec) {
   constexpr int XR = TS::CELLS / TS::R / TS::EPV;  // units per row (CW / EPV)
   constexpr int XU = TS::R * XR;
+  if (!vec) {  // rows not 16-byte aligned (W % (16 / sizeof(T)) != 0): one element per copy
+    constexpr int CW = TS::CELLS / TS::R;
+#pragma unroll
+    for (int u0 = 0; u0 < TS::CELLS; u0 += 32) {
+      const int u = u0 + lane;
+      const int rr = u / CW, cc = u % CW;
+      if (u < TS::CELLS && cc < ncols && r0 + rr < H)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sdst + u * static_cast<uint32_t>(sizeof(T))),
+                     "l"(g + static_cast<size_t>(r0 + rr) * W + cc), "n"(sizeof(T)));
+    }
+    return;
+  }
 #pragma unroll
   for (int u0 = 0; u0 < XU; u0 += 32) {
     const int u = u0 + lane;
@@ -301,8 +313,9 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
 template <typename T, int R>
 __device__ __forceinline__ void prefetch_tile_l2(int lane, int r0, int H, int ncols, int N, size_t WN, int W,
                                                  const T* Bs, const T* Cs, const T* xs, const T* zs,
-                                                 const T* ys) {
-  const int planes = ys != nullptr ? 5 : 4;
+                                                 const T* ys, bool xvec) {
+  // the per-cell planes only when their rows are 16-byte aligned (bulk copies need it)
+  const int planes = !xvec ? 2 : ys != nullptr ? 5 : 4;
   if (lane < planes * R) {
     const int r = r0 + lane % R, k = lane / R;
     if (r < H) {
@@ -478,6 +491,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
   const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
   const uint32_t sbase = smem_u32(sm);
+  const bool xrow16 = a.xvec != 0;  // x / z rows 16-byte aligned
 
   const bool save = a.ckpt != nullptr;
   const int nq = a.plan.nq, nbm1 = a.plan.nb - 1;  // checkpoints every R rows (plan.K == R)
@@ -500,27 +514,30 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   const int ntiles = (H + R - 1) / R;
   int sc = 0;  // slot holding this tile's C; sc+1: hh of this tile; sc+2: C of the next tile
   issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, 0, H, WN, ncols, lane);
-  issue_cells<TS>(sbase + TS::F_X * ES, xg, 0, H, W, ncols, lane);
-  issue_cells<TS>(sbase + TS::F_Z * ES, zg, 0, H, W, ncols, lane);
+  issue_cells<TS>(sbase + TS::F_X * ES, xg, 0, H, W, ncols, lane, xrow16);
+  issue_cells<TS>(sbase + TS::F_Z * ES, zg, 0, H, W, ncols, lane, xrow16);
   cp_async_commit();
   T bc[CW][SH];
   load_b_rows<T, CW, SH>(bc, Bg, r1, H, WN, ncols, N);
 
-  const int pft = a.plan.pft_f;
+  const int pft = a.plan.pf_all ? 0 : a.plan.pft_f;
+  if (a.plan.pf_all)
+    for (int t2 = 1; t2 < ntiles; ++t2)
+      prefetch_tile_l2<T, R>(lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr, xrow16);
   for (int t = 0; t < ntiles; ++t) {
     const int r0 = t * R;
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
 #ifndef S2D_NO_PF
     if (pft > 0 && t + pft < ntiles)
-      prefetch_tile_l2<T, R>(lane, r0 + pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr);
+      prefetch_tile_l2<T, R>(lane, r0 + pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr, xrow16);
 #endif
     // ---- prefetch tile t+1: C into the free slot, x / z into the other parity
     //      (its B operand is loaded into the same registers right after phase 1)
     if (t + 1 < ntiles) {
       issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, r0 + R, H, WN, ncols, lane);
-      issue_cells<TS>(sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg, r0 + R, H, W, ncols, lane);
-      issue_cells<TS>(sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, r0 + R, H, W, ncols, lane);
+      issue_cells<TS>(sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg, r0 + R, H, W, ncols, lane, xrow16);
+      issue_cells<TS>(sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, r0 + R, H, W, ncols, lane, xrow16);
     }
     cp_async_commit();
     const int i1 = r0 + r1;
@@ -692,6 +709,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
   const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
   const uint32_t sbase = smem_u32(sm);
+  const bool xrow16 = a.xvec != 0;  // x / z / dy rows 16-byte aligned
 
   const int nq = a.plan.nq, nbm1 = a.plan.nb - 1;
   const bool has_pred = wpos > 0, has_succ = wpos + 1 < ge.wreal;
@@ -727,9 +745,9 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     const int rl = (ntiles - 1) * R;
     const int par = (ntiles - 1) & 1;
     issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, rl, H, WN, ncols, lane);
-    issue_cells<TS>(sbase + (TS::B_X + par * CELLS) * ES, xg, rl, H, W, ncols, lane);
-    issue_cells<TS>(sbase + (TS::B_Z + par * CELLS) * ES, zg, rl, H, W, ncols, lane);
-    issue_cells<TS>(sbase + (TS::B_Y + par * CELLS) * ES, yg, rl, H, W, ncols, lane);
+    issue_cells<TS>(sbase + (TS::B_X + par * CELLS) * ES, xg, rl, H, W, ncols, lane, xrow16);
+    issue_cells<TS>(sbase + (TS::B_Z + par * CELLS) * ES, zg, rl, H, W, ncols, lane, xrow16);
+    issue_cells<TS>(sbase + (TS::B_Y + par * CELLS) * ES, yg, rl, H, W, ncols, lane, xrow16);
     cp_async_commit();
   }
   T bc[CW][SH];
@@ -742,13 +760,16 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     if (has_pred && ib < H) ldg_states<T, SH>(hh0n, hc_in + static_cast<size_t>(ib) * N);
   }
 
-  const int pft = a.plan.pft_b;
+  const int pft = a.plan.pf_all ? 0 : a.plan.pft_b;
+  if (a.plan.pf_all)
+    for (int t2 = ntiles - 2; t2 >= 0; --t2)
+      prefetch_tile_l2<T, R>(lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
   for (int t = ntiles - 1; t >= 0; --t) {
     const int u = ntiles - 1 - t;  // visiting index (ring phase)
     const int r0 = t * R;
 #ifndef S2D_NO_PF
     if (pft > 0 && t - pft >= 0)
-      prefetch_tile_l2<T, R>(lane, r0 - pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg);
+      prefetch_tile_l2<T, R>(lane, r0 - pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
 #endif
     const int rows = min(R, H - r0);
     const int par = t & 1;
@@ -758,9 +779,9 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     if (t > 0) {
       const int ru = r0 - R;
       issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
-      issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane);
-      issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane);
-      issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane);
+      issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane, xrow16);
+      issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane, xrow16);
+      issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane, xrow16);
     }
     cp_async_commit();
     const int i1 = r0 + r1;

@@ -371,21 +371,28 @@ def test_naive_comparator_vs_oracle(orc, s2d):
     assert rel_error(_variant(s2d, b, nat.VARIANT_NAIVE, torch.float64), oracle_fwd(orc, b, "f64")) <= F64_Y_GATE
 
 
-def test_flat1d_comparator_vs_sequential(orc, s2d):
+@pytest.mark.parametrize("S,H,W,N,dt", [(2, 5, 8, 3, "f64"), (2, 30, 40, 16, "f64"), (3, 14, 14, 16, "f64"),
+                                         (2, 23, 29, 4, "f64"), (2, 56, 56, 16, "f32"), (1, 1, 1, 1, "f64"),
+                                         (2, 7, 73, 8, "f32")])
+def test_flat1d_comparator_vs_sequential(orc, s2d, S, H, W, N, dt):
     """block_scan_1d_forward == scan_1d_sequential on the row-major flattening
-    (test_engine.cpp:75-82)."""
+    (test_engine.cpp:75-82); N in {1, 2, 4, 8, 16} runs the block-scan kernel
+    (chunk boundaries at 512 elements), other N the sequential one."""
     from paper_2412_00678_b200 import _native as nat
 
-    b = make_batch(orc, 2, 5, 8, 3, seed0=47, dtype="f64")
-    y = _variant(s2d, b, nat.VARIANT_FLAT1D, torch.float64)
+    b = make_batch(orc, S, H, W, N, seed0=47, dtype=dt)
+    y = _variant(s2d, b, nat.VARIANT_FLAT1D, torch.float64 if dt == "f64" else torch.float32)
+    gate = 1e-12 if dt == "f64" else 1e-4
     for s in range(b.S):
         L = b.H * b.W
         x, z = b.x[s].ravel(), b.z[s].ravel()
         B, Cc = b.B[s].reshape(L, b.N), b.C[s].reshape(L, b.N)
-        delta = np.where(z + b.bias[s] > 20, z + b.bias[s], np.log1p(np.exp(z + b.bias[s])))
+        x, z, B, Cc = [np.asarray(v, np.float64) for v in (x, z, B, Cc)]
+        A, D, bias = np.asarray(b.A[s], np.float64), float(b.D[s]), float(b.bias[s])
+        delta = np.where(z + bias > 20, z + bias, np.log1p(np.exp(z + bias)))
         h = np.zeros(b.N)
         ref = np.empty(L)
         for k in range(L):
-            h = np.exp(delta[k] * b.A[s]) * h + delta[k] * B[k] * x[k]
-            ref[k] = (Cc[k] * h).sum() + b.D[s] * x[k]
-        assert rel_error(y[s].ravel(), ref) <= 1e-12
+            h = np.exp(delta[k] * A) * h + delta[k] * B[k] * x[k]
+            ref[k] = (Cc[k] * h).sum() + D * x[k]
+        assert rel_error(y[s].ravel(), ref) <= gate

@@ -51,8 +51,9 @@ def _check(orc, b, y, grads, dtype, label):
 @pytest.mark.gpu
 @pytest.mark.parametrize("N", [4, 8, 16, 32])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("H,W", [(37, 40), (9, 212), (5, 16)])
+@pytest.mark.parametrize("H,W", [(37, 40), (9, 212), (5, 16), (14, 14), (7, 7), (23, 230)])
 def test_tile_kernels(orc, N, dtype, H, W):
+    """(W % 4 != 0: x / z / dy rows are not 16-byte aligned -> element copies)"""
     S = 3
     b, op, y, grads = _run(orc, S, H, W, N, dtype, seed=77 + N + H)
     plan = op.plan()
