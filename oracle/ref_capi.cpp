@@ -12,10 +12,12 @@
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <sstream>
 #include <thread>
 #include <vector>
 
 #include "scan2d/engine.hpp"
+#include "scan2d/tensor_io.hpp"
 #include "scan2d/fixtures.hpp"
 #include "scan2d/gradcheck.hpp"
 #include "scan2d/math.hpp"
@@ -230,6 +232,47 @@ double ref_batch_f64(std::int64_t S, int P, int G, int h, int w, int n, int t, i
                      const double* dy, double* y, double* dx) {
   return batch_run<double>(S, P, G, h, w, n, t, threads, do_bwd, x, z, b, c, a, d, bias, dy, y,
                            dx);
+}
+
+// T2DM through the reference's own tensor I/O (tensor_io.cpp:78-151): the
+// golden encoder / decoder the repository's format code is checked against.
+std::size_t ref_t2dm_encode(int dtype, int ndim, const std::uint64_t* dims, const void* data, unsigned char* out,
+                            std::size_t cap) {
+  Tensor t;
+  t.dtype = dtype == 1 ? Dtype::f64 : Dtype::f32;
+  t.dims.assign(dims, dims + ndim);
+  const std::size_t n = t.count();
+  if (dtype == 1)
+    t.f64.assign(static_cast<const double*>(data), static_cast<const double*>(data) + n);
+  else
+    t.f32.assign(static_cast<const float*>(data), static_cast<const float*>(data) + n);
+  std::ostringstream os;
+  try {
+    write_tensor(t, os);
+  } catch (...) {
+    return 0;
+  }
+  const std::string b = os.str();
+  if (b.size() > cap) return 0;
+  std::memcpy(out, b.data(), b.size());
+  return b.size();
+}
+// -1 = decoded (payload copied to out_data when given), else TensorIoError::Kind
+int ref_t2dm_decode(const unsigned char* buf, std::size_t len, std::size_t* offset, void* out_data) {
+  std::istringstream is(std::string(reinterpret_cast<const char*>(buf), len));
+  try {
+    Tensor t = read_tensor(is);
+    if (out_data) {
+      if (t.dtype == Dtype::f64)
+        std::memcpy(out_data, t.f64.data(), 8 * t.f64.size());
+      else
+        std::memcpy(out_data, t.f32.data(), 4 * t.f32.size());
+    }
+    return -1;
+  } catch (const TensorIoError& e) {
+    *offset = e.offset;
+    return static_cast<int>(e.kind);
+  }
 }
 
 // Every gradient group per scan (P == S, G == 1; the bench's parity report).
