@@ -309,9 +309,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=0, help="0 = library heuristic")
     ap.add_argument("--rowband", action="store_true",
-                    help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), "
-                         "vertical carries exchanged point to point, pipelined over scan chunks")
-    ap.add_argument("--chunks", type=int, default=8, help="scan chunks of the row-band pipeline")
+                    help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), vertical "
+                         "carries handed to the neighbouring GPU by the kernels (NVLink peer stores + flags)")
     ap.add_argument("--compare", action="store_true",
                     help="Table 3: tiled vs naive-2D vs flat-1D operators at 14^2/56^2/200^2, D=1 N=16")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
@@ -627,50 +626,41 @@ def max_over_ranks(torch, dist, dev, vals):
 
 def rowband_main(args, wl, rank, world, local, config):
     """Row-band shard: rank r owns rows row_band(H, world, r) of every
-    scan; carries move r -> r+1 (forward) and r+1 -> r (backward) as NCCL
-    send/recv over NVLink, pipelined over scan chunks."""
+    scan on its own GPU (LinkedRowBands): the kernels hand the vertical carries
+    to the neighbouring GPU themselves -- forward h of the band's last row into
+    rank r+1's buffer, backward Abar G of its first row into rank r-1's, over
+    NVLink peer memory (CUDA IPC), with one system-scope release/acquire flag
+    per (scan, 16-column strip).  No collective and no host step on the data
+    path; ranks only meet at a barrier between forward-only steps (the
+    ordering a receive buffer needs, LinkedRowBands docstring)."""
     import torch
 
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("SCAN2D_BENCH_SHARED_GPU") == "1":
+            dist.init_process_group("gloo")
+            local = 0
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    from paper_2412_00678_b200.api import Scan2dBandOp
-    from paper_2412_00678_b200.launcher import RowBandPipeline, band_align, row_band
+    from paper_2412_00678_b200.launcher import LinkedRowBands
 
     S, H, W, N = wl["S"], wl["H"], wl["W"], wl["N"]
-    band = row_band(H, world, rank, band_align(N))
-    nch = max(1, min(args.chunks, S))
-    cs = -(-S // nch)
-    sizes = [min(cs, S - k * cs) for k in range(nch) if k * cs < S]
-    chunks, dys, ops = [], [], []
-    for k, sk in enumerate(sizes):
-        bw = dict(wl, S=sk, H=band.rows)
-        ins, dy = synth_inputs(torch, bw, dev, 1234 + 97 * k + rank, torch.float32)
-        chunks.append(tuple(ins))
-        dys.append(dy)
-        ops.append(Scan2dBandOp(sk, band.rows, W, N, device=dev, with_backward=wl["bwd"]))
-    pipe = RowBandPipeline(rank, world, dist, streams=[torch.cuda.Stream(dev) for _ in range(len(sizes))])
-    shape = lambda k: (sizes[k], W, N)
-    mk = lambda sh: torch.empty(sh, dtype=torch.float32, device=dev)
-
-    class _Fwd:  # forward-only workloads do not keep outputs per chunk
-        def __init__(self, op):
-            self.op = op
-
-        def forward(self, *ins, h_top=None):
-            return self.op.forward(*ins, h_top=h_top, save=wl["bwd"])
-
-        def backward(self, *a, **k):
-            return self.op.backward(*a, **k)
+    lb = LinkedRowBands(S, H, W, N, rank, world, dist=dist, device=dev, with_backward=wl["bwd"])
+    band = lb.band
+    bw = dict(wl, H=band.rows)
+    ins, dy = synth_inputs(torch, bw, dev, 1234 + rank, torch.float32)
+    lb.op.op.check = False
 
     def step():
-        pipe.forward(lambda k: _Fwd(ops[k]), chunks, shape, mk, keep=False)
+        lb.forward(*ins, save=wl["bwd"])
         if wl["bwd"]:
-            pipe.backward(lambda k: ops[k], chunks, dys, shape, mk, keep=False)
+            lb.backward(*ins, dy)
+        else:
+            lb.step_barrier()
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -685,20 +675,19 @@ def rowband_main(args, wl, rank, world, local, config):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        (ms,) = max_over_ranks(torch, dist, dev, [ms])
         dist.barrier()
     if rank == 0:
         fb, bb = alg_bytes(wl)
-        config.update({"parallelism": f"row-band x{world} (p2p vertical carries, {len(sizes)} scan chunks)",
-                       "band_rows": band.rows})
+        config.update({"parallelism": f"row-band x{world} (in-kernel NVLink carry hand-off, per-strip flags)",
+                       "band_rows": band.rows, "S_global": S, "S_per_gpu": [S] * world})
         line = {"metric": METRIC, "value": S * H * W / (ms * 1e-3) / 1e9, "unit": "Gelem/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (random_instance distribution, generated on device)", "config": config,
                 "hbm_gbs_per_gpu": (fb + (bb if wl["bwd"] else 0)) / world / (ms * 1e-3) / 1e9}
         print(json.dumps(line), flush=True)
+    lb.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0

@@ -142,6 +142,43 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
                          void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip, void* dbias,
                          void* g_top, void* workspace, size_t workspace_bytes, scan2d_stream_t stream);
 
+/* ---- row bands on different GPUs, linked in-kernel ----
+ * The same band entry points with the carry hand-off done by the kernels
+ * themselves: h_bottom (forward) / g_top (backward) may point into the NEXT /
+ * PREVIOUS band's buffer on another GPU (peer memory over NVLink, e.g. from
+ * cudaIpcOpenMemHandle, see scan2d_ipc_*), and every (scan, 16-column strip)
+ * publishes its part with a system-scope release flag.  A strip of the
+ * receiving band waits on its own flag (acquire) just before it first reads
+ * h_top / g_bottom, so bands run concurrently and each strip starts as soon as
+ * the strip above (forward) / below (backward) has finished -- no host
+ * synchronisation, no collective, no scan-chunk pipeline.
+ *   in_flags   [S * strips] flags written by the producing band (NULL: no wait)
+ *   out_flags  [S * strips] flags of the consuming band (NULL: no publish)
+ *   seq        value the flags carry for this call (must change from call to
+ *              call on a link, e.g. a counter; flags start at any other value)
+ * strips = scan2d_band_strips(desc).  A producer that never arrives makes the
+ * waiting strips give up after 10 s (wrong results instead of a hung GPU).
+ * Not for CUDA graph capture (seq is a launch argument). */
+int scan2d_band_strips(const scan2d_desc* desc);
+int scan2d_forward_band_linked(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                               const void* C, const void* A, const void* Dskip, const void* bias,
+                               const void* h_top, void* y, void* h_bottom, void* residual, const int* in_flags,
+                               int* out_flags, int seq, void* workspace, size_t workspace_bytes,
+                               scan2d_stream_t stream);
+int scan2d_backward_band_linked(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                                const void* C, const void* A, const void* Dskip, const void* bias,
+                                const void* h_top, const void* residual, const void* dy, const void* g_bottom,
+                                void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip, void* dbias,
+                                void* g_top, const int* in_flags, int* out_flags, int seq, void* workspace,
+                                size_t workspace_bytes, scan2d_stream_t stream);
+/* CUDA IPC for the links between processes (one per GPU): export a device
+ * pointer as a 64-byte handle of its allocation plus the pointer's offset in
+ * it (caching allocators hand out interior pointers), open a peer's handle in
+ * this process (*dev_ptr = mapped base + offset; *base for scan2d_ipc_close). */
+int scan2d_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t* offset);
+int scan2d_ipc_open(const unsigned char handle[64], uint64_t offset, void** dev_ptr, void** base);
+int scan2d_ipc_close(void* base);
+
 /* ---- host operands (the reference API's contract: Grid<T> data lives in host
  * memory, engine.hpp:88-102) ----
  * One training step -- forward, and backward when dy != NULL -- on HOST

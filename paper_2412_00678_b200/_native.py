@@ -28,6 +28,12 @@ EXPORTED_SYMBOLS = (
     "scan2d_backward",
     "scan2d_forward_band",
     "scan2d_backward_band",
+    "scan2d_band_strips",
+    "scan2d_forward_band_linked",
+    "scan2d_backward_band_linked",
+    "scan2d_ipc_export",
+    "scan2d_ipc_open",
+    "scan2d_ipc_close",
     "scan2d_train_host",
     "scan2d_fwd_f32",
     "scan2d_fwd_f64",
@@ -86,6 +92,18 @@ def _load():
     lib.scan2d_forward_band.restype = C.c_int
     lib.scan2d_backward_band.argtypes = [D] + [P] * 20 + [C.c_size_t, P]
     lib.scan2d_backward_band.restype = C.c_int
+    lib.scan2d_band_strips.argtypes = [D]
+    lib.scan2d_band_strips.restype = C.c_int
+    lib.scan2d_forward_band_linked.argtypes = [D] + [P] * 13 + [C.c_int, P, C.c_size_t, P]
+    lib.scan2d_forward_band_linked.restype = C.c_int
+    lib.scan2d_backward_band_linked.argtypes = [D] + [P] * 21 + [C.c_int, P, C.c_size_t, P]
+    lib.scan2d_backward_band_linked.restype = C.c_int
+    lib.scan2d_ipc_export.argtypes = [P, P, C.POINTER(C.c_uint64)]
+    lib.scan2d_ipc_export.restype = C.c_int
+    lib.scan2d_ipc_open.argtypes = [P, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+    lib.scan2d_ipc_open.restype = C.c_int
+    lib.scan2d_ipc_close.argtypes = [P]
+    lib.scan2d_ipc_close.restype = C.c_int
     lib.scan2d_train_host.argtypes = [D] + [P] * 16 + [C.c_int, P]
     lib.scan2d_train_host.restype = C.c_int
     for name, n_in in (("scan2d_fwd_f32", 12), ("scan2d_fwd_f64", 12)):

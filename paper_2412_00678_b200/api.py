@@ -48,6 +48,15 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _vptr(t):
+    """A tensor, a raw device address (int, e.g. IPC-mapped peer memory) or None."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return C.c_void_p(t)
+    return C.c_void_p(t.data_ptr())
+
+
 def _stream(device: torch.device):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -368,11 +377,26 @@ class Scan2dBandOp:
                    and t.is_contiguous(), f"Scan2dBandOp: {name} must be a contiguous [S,W,N] tensor "
                                           "of the op's dtype on its device")
 
-    def forward(self, x, z, B, C_, A, Dskip, bias, h_top=None, save=True):
+    def forward(self, x, z, B, C_, A, Dskip, bias, h_top=None, save=True, link=None, h_bottom=None):
+        """``link`` = (in_flags, out_flags, seq) selects the in-kernel hand-off
+        (``scan2d_forward_band_linked``): flags as tensors or raw device
+        pointers (ints, e.g. peer memory), ``h_bottom`` a tensor or raw pointer
+        to write the band's last-row carry to (default: this op's buffer)."""
         o = self.op
         if o.check:
             o._operands(x, z, B, C_, A, Dskip, bias)
             self._carry(h_top, "h_top")
+        if link is not None:
+            lin, lout, seq = link
+            hb = self.h_bottom if h_bottom is None else h_bottom
+            rc = nat.lib.scan2d_forward_band_linked(
+                C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A), _ptr(Dskip), _ptr(bias),
+                _ptr(h_top), _ptr(o.y), _vptr(hb), _ptr(o.residual) if save else None, _vptr(lin), _vptr(lout),
+                int(seq), _ptr(o.wsf), o.wsf_bytes, _stream(o.dev))
+            if rc != nat.OK:
+                raise nat.Scan2dError(rc, "scan2d_forward_band_linked")
+            self.launches += nat.lib.scan2d_last_launch_count()
+            return o.y, hb
         rc = nat.lib.scan2d_forward_band(C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
                                          _ptr(Dskip), _ptr(bias), _ptr(h_top), _ptr(o.y), _ptr(self.h_bottom),
                                          _ptr(o.residual) if save else None, _ptr(o.wsf), o.wsf_bytes,
@@ -382,12 +406,27 @@ class Scan2dBandOp:
         self.launches += nat.lib.scan2d_last_launch_count()
         return o.y, self.h_bottom
 
-    def backward(self, x, z, B, C_, A, Dskip, bias, h_top, dy, g_bottom=None):
+    def backward(self, x, z, B, C_, A, Dskip, bias, h_top, dy, g_bottom=None, link=None, g_top=None):
+        """``link`` = (in_flags, out_flags, seq): in-kernel hand-off
+        (``scan2d_backward_band_linked``); ``g_top`` a tensor or raw pointer."""
         o = self.op
         if o.check:
             o._operands(x, z, B, C_, A, Dskip, bias, dy)
             self._carry(h_top, "h_top")
-            self._carry(g_bottom, "g_bottom")
+            if link is None:
+                self._carry(g_bottom, "g_bottom")
+        if link is not None:
+            lin, lout, seq = link
+            gt = self.g_top if g_top is None else g_top
+            rc = nat.lib.scan2d_backward_band_linked(
+                C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A), _ptr(Dskip), _ptr(bias),
+                _ptr(h_top), _ptr(o.residual), _ptr(dy), _vptr(g_bottom), _ptr(o.dx), _ptr(o.dz), _ptr(o.dA),
+                _ptr(o.dB), _ptr(o.dC), _ptr(o.dD), _ptr(o.dbias), _vptr(gt), _vptr(lin), _vptr(lout), int(seq),
+                _ptr(o.wsb), o.wsb_bytes, _stream(o.dev))
+            if rc != nat.OK:
+                raise nat.Scan2dError(rc, "scan2d_backward_band_linked")
+            self.launches += nat.lib.scan2d_last_launch_count()
+            return o.dx, o.dz, o.dA, o.dB, o.dC, o.dD, o.dbias, gt
         rc = nat.lib.scan2d_backward_band(C.byref(o.desc), _ptr(x), _ptr(z), _ptr(B), _ptr(C_), _ptr(A),
                                           _ptr(Dskip), _ptr(bias), _ptr(h_top), _ptr(o.residual), _ptr(dy),
                                           _ptr(g_bottom), _ptr(o.dx), _ptr(o.dz), _ptr(o.dA), _ptr(o.dB),

@@ -3,6 +3,7 @@
 //
 // Validation mirrors require_shapes (proj/src/engine.cpp:21-30) and the tile
 // check (:163-164); the backward's stale-state check mirrors engine.cpp:248-249.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -546,7 +547,8 @@ template <typename T>
 int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void* B, const void* C,
                  const void* A, const void* Dskip, const void* bias, void* y, void* ph, void* pv,
                  void* residual, void* ws, size_t ws_bytes, cudaStream_t stream,
-                 const void* vtop = nullptr, void* vbot = nullptr) {
+                 const void* vtop = nullptr, void* vbot = nullptr, const int* lin = nullptr, int* lout = nullptr,
+                 int lseq = 0) {
   g_last_launches = 0;
   if (!x || !z || !B || !C || !A || !Dskip || !bias || !y) return SCAN2D_EINVAL;
   if ((ph == nullptr) != (pv == nullptr)) return SCAN2D_EINVAL;
@@ -571,6 +573,10 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   if ((vtop != nullptr || vbot != nullptr) && !p.f.tile) return SCAN2D_EUNSUPPORTED;
   a.vtop = static_cast<const T*>(vtop);
   a.vbot = static_cast<T*>(vbot);
+  if ((lin != nullptr || lout != nullptr) && !p.f.tile) return SCAN2D_EUNSUPPORTED;
+  a.link_in = lin;
+  a.link_out = lout;
+  a.link_seq = lseq;
   a.hdr = reinterpret_cast<s2d::WsHdr*>(w + L.ticket);
   a.ticket = &a.hdr->ticket;
   if (residual != nullptr) {
@@ -609,7 +615,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
                   const void* residual, const void* dy, void* dx, void* dz, void* dA, void* dB,
                   void* dC, void* dDskip, void* dbias, void* ws, size_t ws_bytes,
                   cudaStream_t stream, const void* vtop = nullptr, const void* gbot = nullptr,
-                  void* gtop = nullptr) {
+                  void* gtop = nullptr, const int* lin = nullptr, int* lout = nullptr, int lseq = 0) {
   g_last_launches = 0;
   if (residual == nullptr) return SCAN2D_ESTALE;
   if (!x || !z || !B || !C || !A || !Dskip || !bias || !dy) return SCAN2D_EINVAL;
@@ -647,6 +653,10 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   a.vtop = static_cast<const T*>(vtop);
   a.gbot = static_cast<const T*>(gbot);
   a.gtop = static_cast<T*>(gtop);
+  if ((lin != nullptr || lout != nullptr) && !p.b.tile) return SCAN2D_EUNSUPPORTED;
+  a.link_in = lin;
+  a.link_out = lout;
+  a.link_seq = lseq;
   a.dx = static_cast<T*>(dx);
   a.dz = static_cast<T*>(dz);
   T* dB_ps = static_cast<T*>(dB);
@@ -804,6 +814,85 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
                                  dbias, workspace, workspace_bytes, st, h_top, g_bottom, g_top);
   return backward_impl<float>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip,
                               dbias, workspace, workspace_bytes, st, h_top, g_bottom, g_top);
+}
+
+int scan2d_band_strips(const scan2d_desc* desc) {
+  if (check_desc(desc) != SCAN2D_OK) return 0;
+  return static_cast<int>(ceil_div(desc->width, tile_cw()));
+}
+
+int scan2d_forward_band_linked(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                               const void* C, const void* A, const void* Dskip, const void* bias,
+                               const void* h_top, void* y, void* h_bottom, void* residual, const int* in_flags,
+                               int* out_flags, int seq, void* workspace, size_t workspace_bytes,
+                               scan2d_stream_t stream) {
+  const int rc = check_desc(desc);
+  if (rc != SCAN2D_OK) return rc;
+  if (desc->state_dim > kMaxKernelN) return SCAN2D_EUNSUPPORTED;
+  if (tile_cw_bwd(*desc, tile_sh(*desc)) != tile_cw()) return SCAN2D_EUNSUPPORTED;  // one strip grid both ways
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (desc->dtype == SCAN2D_F64)
+    return forward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, y, nullptr, nullptr, residual, workspace,
+                                workspace_bytes, st, h_top, h_bottom, in_flags, out_flags, seq);
+  return forward_impl<float>(*desc, x, z, B, C, A, Dskip, bias, y, nullptr, nullptr, residual, workspace,
+                             workspace_bytes, st, h_top, h_bottom, in_flags, out_flags, seq);
+}
+
+int scan2d_backward_band_linked(const scan2d_desc* desc, const void* x, const void* z, const void* B,
+                                const void* C, const void* A, const void* Dskip, const void* bias,
+                                const void* h_top, const void* residual, const void* dy, const void* g_bottom,
+                                void* dx, void* dz, void* dA, void* dB, void* dC, void* dDskip, void* dbias,
+                                void* g_top, const int* in_flags, int* out_flags, int seq, void* workspace,
+                                size_t workspace_bytes, scan2d_stream_t stream) {
+  const int rc = check_desc(desc);
+  if (rc != SCAN2D_OK) return rc;
+  if (desc->state_dim > kMaxKernelN) return SCAN2D_EUNSUPPORTED;
+  if (tile_cw_bwd(*desc, tile_sh(*desc)) != tile_cw()) return SCAN2D_EUNSUPPORTED;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (desc->dtype == SCAN2D_F64)
+    return backward_impl<double>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip,
+                                 dbias, workspace, workspace_bytes, st, h_top, g_bottom, g_top, in_flags,
+                                 out_flags, seq);
+  return backward_impl<float>(*desc, x, z, B, C, A, Dskip, bias, residual, dy, dx, dz, dA, dB, dC, dDskip, dbias,
+                              workspace, workspace_bytes, st, h_top, g_bottom, g_top, in_flags, out_flags, seq);
+}
+
+int scan2d_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t* offset) {
+  if (dev_ptr == nullptr || handle == nullptr || offset == nullptr) return SCAN2D_EINVAL;
+  // the driver's cuMemGetAddressRange through the runtime's entry-point query
+  // (no link-time dependency on libcuda)
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (get_range == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return SCAN2D_ECUDA;
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) return SCAN2D_ECUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return SCAN2D_ECUDA;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  *offset = static_cast<uint64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return SCAN2D_OK;
+}
+
+int scan2d_ipc_open(const unsigned char handle[64], uint64_t offset, void** dev_ptr, void** base) {
+  if (dev_ptr == nullptr || handle == nullptr || base == nullptr) return SCAN2D_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  if (cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return SCAN2D_ECUDA;
+  *dev_ptr = static_cast<unsigned char*>(*base) + offset;
+  return SCAN2D_OK;
+}
+
+int scan2d_ipc_close(void* base) {
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? SCAN2D_OK : SCAN2D_ECUDA;
 }
 
 int scan2d_fwd_f32(const scan2d_desc* desc, const float* x, const float* z, const float* B,

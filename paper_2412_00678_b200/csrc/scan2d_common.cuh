@@ -155,6 +155,40 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
   }
 }
 
+// Band hand-off flags at system scope (the producer may be another GPU).
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait (lane 0 polls, the warp follows) until *flag == seq.  A producer that
+// never arrives (a misconfigured link) must not hang the GPU: after 10 s the
+// wait gives up and the strip proceeds with whatever the carry buffer holds.
+__device__ __forceinline__ void link_wait(const int* flag, int seq, int lane) {
+  if (lane == 0) {
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flag) != seq) {
+      __nanosleep(200);
+      if (global_ns() - t0 > 10000000000ull) break;
+    }
+  }
+  __syncwarp();
+}
+// Publish: every lane's carry stores are made visible system-wide first.
+__device__ __forceinline__ void link_post(int* flag, int seq, int lane) {
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) st_release_sys(flag, seq);
+}
+
 // Pause between polls of a carry word.  __nanosleep deschedules the warp for
 // far longer than asked on sm_100 when the word is not ready yet (one global
 // hop between two CTAs measured 2.2x slower with it); a short clock spin keeps
@@ -555,6 +589,14 @@ struct Args {
   T* vbot;              // forward: h of the band's last row, [S][W][N] (NULL = not wanted)
   const T* gbot;        // backward: Abar G of the row below the band, [S][W][N] (NULL = zeros)
   T* gtop;              // backward: Abar G of the band's first row, [S][W][N] (NULL = not wanted)
+  // in-kernel hand-off between bands on different GPUs (scan2d_*_band_linked):
+  // per (scan, 16-column strip) flags; a strip waits until link_in[s][strip]
+  // == link_seq before reading its incoming carry (vtop forward, gbot
+  // backward) and publishes link_out[s][strip] = link_seq after storing its
+  // outgoing carry (vbot / gtop, typically peer memory over NVLink)
+  const int* link_in;
+  int* link_out;
+  int link_seq;
   CarrySlot<T>* hcarry; // forward chain: tagged horizontal carries at Q-column boundaries, [S][nq][H][N]
   T* hres;              // residual: plain horizontal carries at every Q-column boundary, [S][nq][H][N]
   // backward outputs

@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   T hv[SV];  // vertical state: zeros, or the row above the band (row-band shard)
 #pragma unroll
   for (int e = 0; e < SV; ++e) hv[e] = T(0);
+  if (a.link_in != nullptr) link_wait(a.link_in + s * ge.wreal + wpos, a.link_seq, lane);
   if (a.vtop != nullptr && col_ok) cv.ldg(hv, a.vtop + (s * W + jg2) * N + s2 * SV);
 
   const int ntiles = (H + R - 1) / R;
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
     __syncwarp();
     sc = sn;
   }
+  if (a.link_out != nullptr) link_post(a.link_out + s * ge.wreal + wpos, a.link_seq, lane);
 }
 
 // ================================================================= backward
@@ -732,6 +734,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   T dn[SV];  // Abar(i+1,j) G(i+1,j), carried up across tiles (column lanes)
 #pragma unroll
   for (int e = 0; e < SV; ++e) dn[e] = T(0);
+  if (a.link_in != nullptr) link_wait(a.link_in + s * ge.wreal + wpos, a.link_seq, lane);
   if (a.gbot != nullptr && col_ok) cv.ldg(dn, a.gbot + (s * W + jg2) * N + s2 * SV);
   T dAr[SH];
 #pragma unroll
@@ -1004,6 +1007,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
 
   if (a.gtop != nullptr && col_ok)  // row-band shard: the band above continues from here
     cv.stg(a.gtop + (s * W + jg2) * N + s2 * SV, dn);
+  if (a.link_out != nullptr) link_post(a.link_out + s * ge.wreal + wpos, a.link_seq, lane);
 
   // ---- per-(scan, strip) partials, fixed order: dA = row-lane part + column-lane part
 #pragma unroll

@@ -301,3 +301,130 @@ def reduce_params(dist, parts, world: int):
             acc += b
         out.append(acc)
     return out
+
+
+class LinkedRowBands:
+    """Row-band shard with the carry hand-off done inside the kernels
+    (``scan2d_forward_band_linked`` / ``scan2d_backward_band_linked``; SURVEY.md
+    §8e): rank r owns rows ``row_band(H, world, r, band_align(N))`` of all S
+    scans on its own GPU.
+
+    Setup (off the hot path): every rank allocates its receive buffers --
+    ``h_top`` [S,W,N] plus forward flags (written by rank r-1) and ``g_bottom``
+    [S,W,N] plus backward flags (written by rank r+1) -- exports them as CUDA
+    IPC handles, all-gathers the handles over ``dist`` and opens its
+    neighbours'.  A forward then stores each (scan, 16-column strip)'s last-row
+    state straight into rank r+1's ``h_top`` over NVLink and releases rank
+    r+1's flag for that strip; rank r+1's strip acquires the flag right before
+    it first reads ``h_top``.  The backward does the same upwards with
+    ``Abar G``.  Per call: kernels only -- no host synchronisation, no
+    collective, no scan-chunk pipeline; strips start as soon as their
+    producer strip is done.
+
+    Ordering across calls: a producer must not overwrite a receive buffer
+    before the consumer has read it.  In a training step (forward, then
+    backward) the backward's reverse hand-off orders the next forward after
+    the consumer's forward; forward-only loops call ``step_barrier()``
+    between steps."""
+
+    def __init__(self, S, H, W, N, rank, world, dist=None, device="cuda", dtype=None, with_backward=True):
+        import torch
+
+        from . import _native as nat
+        from .api import Scan2dBandOp
+
+        self.nat, self.torch = nat, torch
+        self.rank, self.world, self.dist = rank, world, dist
+        dtype = torch.float32 if dtype is None else dtype
+        self.band = row_band(H, world, rank, band_align(N, 4 if dtype == torch.float32 else 8))
+        self.S, self.W, self.N = S, W, N
+        self.op = Scan2dBandOp(S, self.band.rows, W, N, dtype=dtype, device=device, with_backward=with_backward)
+        self.strips = nat.lib.scan2d_band_strips(ctypes_byref(self.op.desc))
+        dev = self.op.op.dev
+        self.h_top = torch.zeros((S, W, N), dtype=dtype, device=dev) if rank > 0 else None
+        self.g_bottom = torch.zeros((S, W, N), dtype=dtype, device=dev) if rank < world - 1 else None
+        self.f_in = torch.zeros(S * self.strips, dtype=torch.int32, device=dev) if rank > 0 else None
+        self.b_in = torch.zeros(S * self.strips, dtype=torch.int32, device=dev) if rank < world - 1 else None
+        self._opened = []
+        self.peer = {"h_next": None, "f_next": None, "g_prev": None, "b_prev": None}
+        if world > 1:
+            mine = {k: (self._export(t) if t is not None else None)
+                    for k, t in (("h_top", self.h_top), ("f_in", self.f_in), ("g_bottom", self.g_bottom),
+                                 ("b_in", self.b_in))}
+            allh = [None] * world
+            dist.all_gather_object(allh, mine)
+            if rank < world - 1:
+                self.peer["h_next"] = self._open(allh[rank + 1]["h_top"])
+                self.peer["f_next"] = self._open(allh[rank + 1]["f_in"])
+            if rank > 0:
+                self.peer["g_prev"] = self._open(allh[rank - 1]["g_bottom"])
+                self.peer["b_prev"] = self._open(allh[rank - 1]["b_in"])
+        self.seq_f = 0
+        self.seq_b = 0
+
+    def _export(self, t):
+        import ctypes as C
+
+        h = (C.c_ubyte * 64)()
+        off = C.c_uint64(0)
+        rc = self.nat.lib.scan2d_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off))
+        if rc != self.nat.OK:
+            raise self.nat.Scan2dError(rc, "scan2d_ipc_export")
+        return bytes(h), off.value
+
+    def _open(self, exported):
+        import ctypes as C
+
+        handle, off = exported
+        p, base = C.c_void_p(), C.c_void_p()
+        rc = self.nat.lib.scan2d_ipc_open((C.c_ubyte * 64).from_buffer_copy(handle), off, C.byref(p), C.byref(base))
+        if rc != self.nat.OK:
+            raise self.nat.Scan2dError(rc, "scan2d_ipc_open")
+        self._opened.append(base.value)
+        return p.value
+
+    def views(self, x, z, B, C, dy=None):
+        """This rank's rows of the global per-cell operands."""
+        r0, r1 = self.band.r0, self.band.r1
+        out = [t[:, r0:r1].contiguous() for t in (x, z, B, C)]
+        if dy is not None:
+            out.append(dy[:, r0:r1].contiguous())
+        return out
+
+    def forward(self, x, z, B, C, A, Dskip, bias, save=True):
+        self.seq_f += 1
+        link = (self.f_in, self.peer["f_next"], self.seq_f)
+        y, _ = self.op.forward(x, z, B, C, A, Dskip, bias, h_top=self.h_top, save=save, link=link,
+                               h_bottom=self.peer["h_next"])
+        return y
+
+    def backward(self, x, z, B, C, A, Dskip, bias, dy):
+        """Gradients of this band; dA / dDskip / dbias are band partial sums
+        (``reduce_params`` adds them over ranks in rank order)."""
+        self.seq_b += 1
+        link = (self.b_in, self.peer["b_prev"], self.seq_b)
+        out = self.op.backward(x, z, B, C, A, Dskip, bias, self.h_top, dy, g_bottom=self.g_bottom, link=link,
+                               g_top=self.peer["g_prev"])
+        return out[:-1]
+
+    def step_barrier(self):
+        self.torch.cuda.current_stream(self.op.op.dev).synchronize()
+        if self.dist is not None and self.world > 1:
+            self.dist.barrier()
+
+    def close(self):
+        for p in self._opened:
+            self.nat.lib.scan2d_ipc_close(ctypes_vp(p))
+        self._opened = []
+
+
+def ctypes_byref(x):
+    import ctypes as C
+
+    return C.byref(x)
+
+
+def ctypes_vp(p):
+    import ctypes as C
+
+    return C.c_void_p(p)

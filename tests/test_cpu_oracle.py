@@ -176,6 +176,15 @@ def test_capi_exports_every_header_symbol():
     assert sorted(_native.EXPORTED_SYMBOLS) == names
 
 
+def test_t2dm_exports_every_header_symbol():
+    lib = C.CDLL(LIB)
+    txt = re.sub(r"/\*.*?\*/", "", open(os.path.join(os.path.dirname(HEADER), "scan2d_t2dm.h")).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(scan2d_t2dm_[a-z0-9_]+)\s*\(", txt)))
+    assert len(names) == 7
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in include/scan2d_t2dm.h but not exported"
+
+
 def test_capi_descriptor_validation():
     from paper_2412_00678_b200 import _native as nat
 

@@ -172,3 +172,112 @@ def test_cuda_band_chain_bitwise(dtype):
     for idx in (2, 5, 6):
         tot = outs[0][idx] + outs[1][idx] + outs[2][idx]
         assert rel_error(tot.cpu().numpy(), g_full[idx].cpu().numpy()) < (1e-5 if dtype == "f32" else 1e-12)
+
+
+def _full_and_bands(dtype, S, H, W, N, nb, seed):
+    from paper_2412_00678_b200.api import Scan2dOp
+    from scan_cases import batch_to_torch
+
+    orc = Oracle()
+    b = make_batch(orc, S, H, W, N, seed0=seed, dtype=dtype)
+    (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    full = Scan2dOp(S, H, W, N, dtype=x.dtype, device="cuda")
+    y_full = full.forward(x, z, B, C, A, D, bias).clone()
+    g_full = [t.clone() for t in full.backward(x, z, B, C, A, D, bias, dy)]
+    torch.cuda.synchronize()
+    bands = [row_band(H, nb, r, band_align(N, 4 if dtype == "f32" else 8)) for r in range(nb)]
+    return (x, z, B, C, A, D, bias), dy, y_full, g_full, bands
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_cuda_linked_bands_in_kernel_handoff(dtype):
+    """Three bands on three streams, linked in-kernel (scan2d_*_band_linked):
+    every consumer band is launched BEFORE its producer, so only the per-strip
+    flags order them; y, dx, dz, dB, dC must equal the single-grid run bit for
+    bit, twice in a row (the flags' sequence number advances)."""
+    from paper_2412_00678_b200 import _native as nat
+    from paper_2412_00678_b200.api import Scan2dBandOp
+
+    S, H, W, N = 3, 40, 48, 16
+    (x, z, B, C, A, D, bias), dy, y_full, g_full, bands = _full_and_bands(dtype, S, H, W, N, 3, 700)
+    tdt = x.dtype
+    ops = [Scan2dBandOp(S, bd.rows, W, N, dtype=tdt, device="cuda") for bd in bands]
+    strips = nat.lib.scan2d_band_strips(__import__("ctypes").byref(ops[0].desc))
+    hbuf = [torch.zeros((S, W, N), dtype=tdt, device="cuda") for _ in range(2)]  # band k -> k+1
+    gbuf = [torch.zeros((S, W, N), dtype=tdt, device="cuda") for _ in range(2)]  # band k+1 -> k
+    ff = [torch.zeros(S * strips, dtype=torch.int32, device="cuda") for _ in range(2)]
+    bf = [torch.zeros(S * strips, dtype=torch.int32, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    sl = lambda t, bd: t[:, bd.r0:bd.r1].contiguous()  # noqa: E731
+    ins = [(sl(x, bd), sl(z, bd), sl(B, bd), sl(C, bd), A, D, bias) for bd in bands]
+    dys = [sl(dy, bd) for bd in bands]
+    torch.cuda.synchronize()
+    for seq in (1, 2):
+        for k in (2, 1, 0):  # consumers first
+            with torch.cuda.stream(streams[k]):
+                ops[k].forward(*ins[k], h_top=hbuf[k - 1] if k > 0 else None,
+                               link=(ff[k - 1] if k > 0 else None, ff[k] if k < 2 else None, seq),
+                               h_bottom=hbuf[k] if k < 2 else None)
+        for k in (0, 1, 2):  # backward consumers (upper bands) first
+            with torch.cuda.stream(streams[k]):
+                ops[k].backward(*ins[k], hbuf[k - 1] if k > 0 else None, dys[k],
+                                g_bottom=gbuf[k] if k < 2 else None,
+                                link=(bf[k] if k < 2 else None, bf[k - 1] if k > 0 else None, seq),
+                                g_top=gbuf[k - 1] if k > 0 else None)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.cat([o.op.y for o in ops], dim=1), y_full), seq
+        for idx, name in [(0, "dx"), (1, "dz"), (3, "dB"), (4, "dC")]:
+            got = torch.cat([[o.op.dx, o.op.dz, o.op.dA, o.op.dB, o.op.dC][idx] for o in ops], dim=1)
+            assert torch.equal(got, g_full[idx]), (seq, name)
+        for idx, t in ((2, "dA"), (5, "dD"), (6, "dbias")):
+            parts = [[o.op.dx, o.op.dz, o.op.dA, o.op.dB, o.op.dC, o.op.dD, o.op.dbias][idx] for o in ops]
+            tot = parts[0] + parts[1] + parts[2]
+            assert rel_error(tot.cpu().numpy(), g_full[idx].cpu().numpy()) < (1e-5 if dtype == "f32" else 1e-12), t
+
+
+def _ipc_worker(rank, world, port, path):
+    import torch.distributed as dist
+
+    from paper_2412_00678_b200.launcher import LinkedRowBands
+    from scan_cases import batch_to_torch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    S, H, W, N = 2, 24, 40, 16
+    b = make_batch(Oracle(), S, H, W, N, seed0=710, dtype="f32")
+    (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    lb = LinkedRowBands(S, H, W, N, rank, world, dist=dist, device="cuda:0")
+    xs, zs, Bs, Cs, dys = lb.views(x, z, B, C, dy)
+    for _ in range(2):
+        y = lb.forward(xs, zs, Bs, Cs, A, D, bias).clone()
+        g = [t.clone() for t in lb.backward(xs, zs, Bs, Cs, A, D, bias, dys)]
+        lb.step_barrier()
+    torch.cuda.synchronize()
+    np.savez(f"{path}.{rank}.npz", r0=lb.band.r0, r1=lb.band.r1, y=y.cpu().numpy(),
+             **{k: v.cpu().numpy() for k, v in zip(("dx", "dz", "dA", "dB", "dC", "dD", "dbias"), g)})
+    lb.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_cuda_linked_bands_ipc_two_processes(tmp_path):
+    """Two processes (one band each) linked through CUDA IPC handles exchanged
+    over gloo -- the multi-GPU setup, here with both processes on cuda:0."""
+    import torch.multiprocessing as mp
+
+    S, H, W, N = 2, 24, 40, 16
+    (x, z, B, C, A, D, bias), dy, y_full, g_full, bands = _full_and_bands("f32", S, H, W, N, 2, 710)
+    port = 29700 + os.getpid() % 1000
+    path = str(tmp_path / "ipc")
+    mp.spawn(_ipc_worker, args=(2, port, path), nprocs=2, join=True)
+    parts = [np.load(f"{path}.{r}.npz") for r in range(2)]
+    y = np.concatenate([p["y"] for p in parts], axis=1)
+    assert np.array_equal(y, y_full.cpu().numpy())
+    for idx, k in [(0, "dx"), (1, "dz"), (3, "dB"), (4, "dC")]:
+        assert np.array_equal(np.concatenate([p[k] for p in parts], axis=1), g_full[idx].cpu().numpy()), k
+    for idx, k in [(2, "dA"), (5, "dD"), (6, "dbias")]:
+        assert rel_error(parts[0][k] + parts[1][k], g_full[idx].cpu().numpy()) < 1e-5, k
