@@ -311,6 +311,9 @@ def main():
     ap.add_argument("--rowband", action="store_true",
                     help="row-band shard: every rank owns H/world rows of all S scans (cfg5 mode), vertical "
                          "carries handed to the neighbouring GPU by the kernels (NVLink peer stores + flags)")
+    ap.add_argument("--api", default="cabi", choices=["cabi", "shim"],
+                    help="shim: time the reference's own C++ API (one scan per call, host Grid operands) served "
+                         "by libscan2d_engine_cuda.so over all host cores (lib/bench_shim)")
     ap.add_argument("--compare", action="store_true",
                     help="Table 3: tiled vs naive-2D vs flat-1D operators at 14^2/56^2/200^2, D=1 N=16")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
@@ -319,6 +322,8 @@ def main():
     args = ap.parse_args()
     if args.compare:
         return compare_main(args)
+    if args.api == "shim":
+        return shim_main(args)
     wl = dict(WORKLOADS[args.workload])
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -589,6 +594,31 @@ def compare_main(args):
     print(json.dumps({"compare": "Table 3 (PAPER.md:280-282) on one B200: D=1 N=16 fp32 forward, CUDA-graph "
                                  "replay of 20 calls (device time), inputs L2-resident like the paper's repeated "
                                  "inference calls", "rows": rows}), flush=True)
+    return 0
+
+
+def shim_main(args):
+    """The drop-in path at the reference contract: the workload's scans through
+    scan2d::tiled_scan_2d_forward / tiled_scan_2d_backward (engine.hpp:88-102)
+    with host Grid operands, one call per scan, spread over all host cores --
+    the same call pattern as the reference arm -- served by the CUDA engine
+    shim.  Prints one JSON line with the e2e throughput."""
+    import subprocess
+
+    wl = dict(WORKLOADS[args.workload])
+    exe = os.path.join(REPO, "paper_2412_00678_b200", "lib", "bench_shim")
+    cmd = [exe, "--scans", str(wl["S"]), "--height", str(wl["H"]), "--width", str(wl["W"]),
+           "--state-dim", str(wl["N"]), "--threads", str(os.cpu_count() or 1), "--reps", str(args.steps),
+           "--warmup", str(max(args.warmup, 1))] + ([] if wl["bwd"] else ["--forward-only"])
+    out = json.loads(subprocess.run(cmd, check=True, capture_output=True, text=True).stdout)
+    print(json.dumps({"metric": METRIC, "api": "shim", "value": out["gelem_per_s"], "unit": "Gelem/s",
+                      "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 1),
+                      "ms_per_step": out["seconds_per_pass"] * 1e3, "higher_is_better": True,
+                      "config": {"workload": args.workload, "desc": wl["desc"]},
+                      "e2e": {"value": out["gelem_per_s"], "unit": "Gelem/s",
+                              "h2d_bytes_per_step": out["h2d_bytes_per_pass"],
+                              "d2h_bytes_per_step": out["d2h_bytes_per_pass"]},
+                      "detail": out}), flush=True)
     return 0
 
 

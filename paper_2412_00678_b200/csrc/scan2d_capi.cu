@@ -252,11 +252,10 @@ void vec_flags(const scan2d_desc& d, const Plan& p, const void* x, const void* z
 // Tile-transpose kernels (scan2d_tile2.cuh): N in {4, 8, 16, 32}, 16-byte
 // aligned B / C rows, strips of 16 columns (the carry grid Q becomes 16); x / z
 // / dy rows that are not 16-byte aligned are staged element by element.
-// (Reference CarryState emission -- ph / pv, only the C++ shim asks for it --
-// runs on the warp kernel instead: the residual layout is the same.)
+// They also emit the reference CarryState (ph / pv) when asked.
 bool use_tile_fwd(const scan2d_desc& d, bool xvec, bool bvec, bool emit) {
   (void)xvec;  // x / z / dy rows that are not 16-byte aligned take element copies (issue_cells)
-  if (emit) return false;
+  if (emit && env_int("SCAN2D_TILE_EMIT", 1) != 1) return false;  // (diagnostics: warp-kernel emission)
   const int N = d.state_dim;
   if (!(N == 4 || N == 8 || N == 16 || N == 32) || !bvec) return false;
   return env_int("SCAN2D_TILE_FWD", 1) == 1;

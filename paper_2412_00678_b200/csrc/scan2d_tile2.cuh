@@ -445,7 +445,7 @@ __device__ __forceinline__ StripId strip_id(const Geo& ge, const Args<T>& a, boo
 
 // ================================================================== forward
 
-template <typename T, int N, int CW, int SH>
+template <typename T, int N, int CW, int SH, bool EMIT = false>
 __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel(const Args<T> a) {
   using TS = T2Shape<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
@@ -505,6 +505,10 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   T* hr_out = save && has_succ ? a.hres + ((s * nq + wpos) * H) * N + q1 * SH : nullptr;
   const int jg2 = c0 + j2;
   const bool col_ok = j2 < ncols;
+  // reference CarryState emission (the C++ engine shim asks for it)
+  constexpr bool emit = EMIT;  // (a separate instantiation: no registers spent when off)
+  const int Tt = EMIT ? a.T_tile : 1;
+  const int kht = EMIT ? (H + Tt - 1) / Tt : 1, kwt = EMIT ? (W + Tt - 1) / Tt : 1;
 
   T hv[SV];  // vertical state: zeros, or the row above the band (row-band shard)
 #pragma unroll
@@ -600,6 +604,13 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 #pragma unroll
           for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
           if (j < ncols) sts_vec<T, SH>(hr + j * N, hh);
+          // reference CarryState P^h (engine.cpp:188-194): hh at the last column of
+          // every reference tile (edge slots stay zero, the reference's pass-through)
+          if (emit && row_ok && j < ncols && ((c0 + j) % Tt == Tt - 1 || c0 + j == W - 1)) {
+            const size_t tl = (static_cast<size_t>(s) * kht + i1 / Tt) * kwt + (c0 + j) / Tt;
+#pragma unroll
+            for (int e = 0; e < SH; ++e) a.ph[(tl * Tt + i1 % Tt) * N + q1 * SH + e] = hh[e];
+          }
           // column j is done with B: load the next tile's in place
           if (t + 1 < ntiles && j < ncols && i1 + R < H)
             ldg_states<T, SH>(bc[j], Bg + static_cast<size_t>(i1 + R) * WN + static_cast<size_t>(j) * N);
@@ -646,6 +657,11 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
           }
           if (i == H - 1 && a.vbot != nullptr)  // row-band shard: the next band's vtop
             cv.stg(a.vbot + (s * W + jg2) * N + s2 * SV, hv);
+          if (emit && (i % Tt == Tt - 1 || i == H - 1)) {  // reference CarryState P^v (engine.cpp:217-220)
+            const size_t tl = (static_cast<size_t>(s) * kht + i / Tt) * kwt + jg2 / Tt;
+#pragma unroll
+            for (int e = 0; e < SV; ++e) a.pv[(tl * Tt + jg2 % Tt) * N + s2 * SV + cv.state(e)] = hv[e];
+          }
         }
       }
     }
