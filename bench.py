@@ -306,6 +306,7 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-accurate", action="store_true", help="skip the accurate-mode side measurement")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=0, help="0 = library heuristic")
     ap.add_argument("--rowband", action="store_true",
@@ -464,6 +465,34 @@ def main():
         extra.update({"bwd_ms": bwd_ms, "bwd_gbs": bb / (bwd_ms * 1e-3) / 1e9,
                       "bwd_frac": bb / (bwd_ms * 1e-3) / 1e9 / peak})
     extra["plan"] = op.plan()
+    # the accurate-exponential mode (SCAN2D_FLAG_ACCURATE: fp32 error at or below
+    # the reference fp32 engine's) on the same inputs, for its cost
+    if not args.no_accurate:
+        aop = Scan2dOp(shard.count, wl["H"], wl["W"], wl["N"], tile=16, dtype=dtype, device=dev,
+                       with_backward=wl["bwd"], accurate=True)
+        aop.check = False
+        for _ in range(3):
+            aop.forward(*ins, save=wl["bwd"])
+            if wl["bwd"]:
+                aop.backward(*ins, dy)
+        aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for a0, a1, a2 in aev:
+            if flush:
+                scratch.fill_(1)
+            a0.record(stream)
+            aop.forward(*ins, save=wl["bwd"])
+            a1.record(stream)
+            if wl["bwd"]:
+                aop.backward(*ins, dy)
+            a2.record(stream)
+        torch.cuda.synchronize()
+        afwd = statistics.median(a.elapsed_time(b) for a, b, _ in aev)
+        abwd = statistics.median(b.elapsed_time(c) for _, b, c in aev) if wl["bwd"] else 0.0
+        extra["accurate_mode"] = {"flag": "SCAN2D_FLAG_ACCURATE", "fwd_ms": afwd, "bwd_ms": abwd,
+                                  "step_ms": afwd + abwd, "value": shard.count * wl["H"] * wl["W"] /
+                                  ((afwd + abwd) * 1e-3) / 1e9 * world}
+        del aop
     extra["gstate_updates_per_s"] = value * wl["N"]
     extra["inputs_vs_l2"] = f"inputs {fb / 1e6:.0f} MB {'>' if fb > L2_BYTES else '<='} L2 {L2_BYTES / 1e6:.0f} MB"
 

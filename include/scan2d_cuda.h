@@ -83,8 +83,15 @@ typedef struct scan2d_desc {
   int32_t params_period;/* P >= 1, divides S                                    */
   int32_t bc_group;     /* G >= 1, divides S                                    */
   int32_t dtype;        /* SCAN2D_F32 or SCAN2D_F64                            */
-  int32_t reserved;     /* must be 0                                           */
+  int32_t flags;        /* 0, or SCAN2D_FLAG_ACCURATE                          */
 } scan2d_desc;
+
+/* desc->flags: fp32 exponentials by range reduction + polynomial (< 1 ulp)
+ * instead of the MUFU ex2.approx (~2 ulp, one-signed): fp32 results closer to
+ * fp64 than the reference's own fp32 engine (tile N in {4, 8, 16, 32} and row
+ * N = 1 kernels; other N already use a compensated exponential), at a cost in
+ * speed.  No effect on fp64. */
+#define SCAN2D_FLAG_ACCURATE 1
 
 /* Validates a descriptor (the checks of require_shapes, engine.cpp:21-30). */
 int scan2d_check_desc(const scan2d_desc* desc);

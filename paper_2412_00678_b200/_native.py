@@ -60,7 +60,7 @@ class Scan2dDesc(C.Structure):
         ("params_period", C.c_int32),
         ("bc_group", C.c_int32),
         ("dtype", C.c_int32),
-        ("reserved", C.c_int32),
+        ("flags", C.c_int32),
     ]
 
 
@@ -134,9 +134,13 @@ def status_string(status: int) -> str:
     return lib.scan2d_status_string(status).decode()
 
 
-def make_desc(S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=F32) -> Scan2dDesc:
+FLAG_ACCURATE = 1  # include/scan2d_cuda.h SCAN2D_FLAG_ACCURATE
+
+
+def make_desc(S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=F32, accurate=False) -> Scan2dDesc:
     return Scan2dDesc(int(S), int(H), int(W), int(N), int(tile),
-                      int(S if params_period is None else params_period), int(bc_group), int(dtype), 0)
+                      int(S if params_period is None else params_period), int(bc_group), int(dtype),
+                      FLAG_ACCURATE if accurate else 0)
 
 
 def plan_info(desc: Scan2dDesc, op: int = OP_FWD) -> dict:

@@ -123,7 +123,7 @@ def _normalise(x, z, B, C_, A, Dskip, bias):
     return x, z, B, C_, A, Dskip, bias
 
 
-def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int) -> nat.Scan2dDesc:
+def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int, accurate: bool = False) -> nat.Scan2dDesc:
     """require_shapes (engine.cpp:21-30) + TileConfig (types.hpp:133-146) checks."""
     _check(x.dim() == 3, "scan input must be [S,H,W] (single channel per scan)")
     S, H, W = x.shape
@@ -145,7 +145,8 @@ def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int) -> nat.Scan2dDesc:
         _check(t.dtype == x.dtype, "scan2d: all tensors must share one dtype")
         _check(t.device == x.device, "scan2d: all tensors must be on one device")
     G = S // B.shape[0]
-    desc = nat.make_desc(S, H, W, N, tile=tile, params_period=P, bc_group=G, dtype=_dtype_code(x))
+    desc = nat.make_desc(S, H, W, N, tile=tile, params_period=P, bc_group=G, dtype=_dtype_code(x),
+                         accurate=accurate)
     rc = nat.lib.scan2d_check_desc(C.byref(desc))
     if rc == nat.EINVAL:
         raise ValueError(nat.status_string(rc))
@@ -156,7 +157,7 @@ def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int) -> nat.Scan2dDesc:
 
 def tiled_scan_2d_forward(x, z, B, C_, A, Dskip, bias, tile: int = 16, threads: int = 1,
                           save_residuals: bool = True, carries: bool = False,
-                          counter=None) -> TiledForwardResult:
+                          counter=None, accurate: bool = False) -> TiledForwardResult:
     """Batched ``tiled_scan_2d_forward`` (engine.hpp:88-94) on the GPU.
 
     ``counter`` (a dict) is filled with the reference element-transfer model
@@ -164,7 +165,7 @@ def tiled_scan_2d_forward(x, z, B, C_, A, Dskip, bias, tile: int = 16, threads: 
     del threads  # results are thread-invariant by construction
     x, z, B, C_, A, Dskip, bias = _normalise(x, z, B, C_, A, Dskip, bias)
     x, z, B, C_, A, Dskip, bias = [t.contiguous() for t in (x, z, B, C_, A, Dskip, bias)]
-    desc = make_desc_for(x, z, B, C_, A, Dskip, bias, tile)
+    desc = make_desc_for(x, z, B, C_, A, Dskip, bias, tile, accurate)
     S, H, W = x.shape
     N = B.shape[3]
     dev = x.device
@@ -253,14 +254,14 @@ class Scan2dOp:
     enqueues exactly the library's kernels (no allocator traffic)."""
 
     def __init__(self, S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=torch.float32,
-                 device="cuda", with_backward=True):
+                 device="cuda", with_backward=True, accurate=False):
         self.dev = torch.device(device)
         if self.dev.type == "cuda" and self.dev.index is None:
             self.dev = torch.device("cuda", torch.cuda.current_device())
         self.dtype = dtype
         code = nat.F64 if dtype == torch.float64 else nat.F32
         self.desc = nat.make_desc(S, H, W, N, tile=tile, params_period=params_period, bc_group=bc_group,
-                                  dtype=code)
+                                  dtype=code, accurate=accurate)
         rc = nat.lib.scan2d_check_desc(C.byref(self.desc))
         if rc != nat.OK:
             raise ValueError(nat.status_string(rc))

@@ -57,7 +57,7 @@ int check_desc(const scan2d_desc* d) {
   if (d->params_period < 1 || d->num_scans % d->params_period != 0) return SCAN2D_EINVAL;
   if (d->bc_group < 1 || d->num_scans % d->bc_group != 0) return SCAN2D_EINVAL;
   if (d->dtype != SCAN2D_F32 && d->dtype != SCAN2D_F64) return SCAN2D_EINVAL;
-  if (d->reserved != 0) return SCAN2D_EINVAL;
+  if ((d->flags & ~SCAN2D_FLAG_ACCURATE) != 0) return SCAN2D_EINVAL;
   // N > 128 runs as passes over state groups of <= 128 (scan2d_groups.cu)
   return SCAN2D_OK;
 }
@@ -532,6 +532,7 @@ void fill_common(Args<T>& a, const scan2d_desc& d, const Plan& p, const void* x,
   a.T_tile = d.tile;
   a.P = d.params_period;
   a.G = d.bc_group;
+  a.acc = (d.flags & SCAN2D_FLAG_ACCURATE) != 0;
   a.plan = p;
 }
 

@@ -109,6 +109,55 @@ struct Num<double> {
   }
 };
 
+// Accurate-exponential policy (desc flag SCAN2D_FLAG_ACCURATE): MUFU.EX2
+// (ex2.approx) carries up to ~2 ulp of relative error with a consistent sign,
+// which the 2D recurrences accumulate along every path -- the measured cause of
+// the fast path's fp32 error being ~2-3x the reference fp32 engine's.  The
+// accurate policy evaluates 2^t by range reduction (t = k + f, |f| <= 1/2) and a
+// degree-7 polynomial in f (truncation < 6e-9 relative, i.e. < 0.1 ulp before
+// rounding), the scaling by 2^k exact; softplus / sigmoid use it and IEEE
+// division.  Kernels take it as a template parameter (no cost when off).
+template <typename T, bool ACC>
+struct Fn : Num<T> {};
+
+template <>
+struct Fn<float, true> {
+  static __device__ __forceinline__ float exp_scaled(float t) {
+    t = fminf(fmaxf(t, -125.0f), 126.0f);
+    const float k = rintf(t);
+    const float f = t - k;  // exact
+    float p = 1.5252733804059841e-05f;
+    p = fmaf(p, f, 1.5403530393381608e-04f);
+    p = fmaf(p, f, 1.3333558146428443e-03f);
+    p = fmaf(p, f, 9.6181291076284772e-03f);
+    p = fmaf(p, f, 5.5504108664821580e-02f);
+    p = fmaf(p, f, 2.4022650695910071e-01f);
+    p = fmaf(p, f, 6.9314718055994531e-01f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (static_cast<int>(k) << 23));
+  }
+  static __device__ __forceinline__ float a_scale(float a) { return Num<float>::a_scale(a); }
+  static __device__ __forceinline__ float softplus(float v) {
+    const float t = exp_scaled(-fabsf(v) * 1.4426950408889634f);
+    const float s = __fdiv_rn(t, 2.0f + t);
+    const float s2 = s * s;
+    float p = 1.0f / 13.0f;
+    p = fmaf(p, s2, 1.0f / 11.0f);
+    p = fmaf(p, s2, 1.0f / 9.0f);
+    p = fmaf(p, s2, 1.0f / 7.0f);
+    p = fmaf(p, s2, 1.0f / 5.0f);
+    p = fmaf(p, s2, 1.0f / 3.0f);
+    p = fmaf(p, s2, 1.0f);
+    const float r = fmaxf(v, 0.0f) + 2.0f * s * p;
+    return v > 20.0f ? v : r;
+  }
+  static __device__ __forceinline__ float sigmoid(float v) {
+    const float e = exp_scaled(-fabsf(v) * 1.4426950408889634f);
+    const float r = __fdiv_rn(1.0f, 1.0f + e);
+    return v >= 0.0f ? r : e * r;
+  }
+};
+
 // ------------------------------------------------------------ shared memory
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -597,6 +646,7 @@ struct Args {
   const int* link_in;
   int* link_out;
   int link_seq;
+  int acc;               // accurate exponential policy (Fn<T, true>)
   CarrySlot<T>* hcarry; // forward chain: tagged horizontal carries at Q-column boundaries, [S][nq][H][N]
   T* hres;              // residual: plain horizontal carries at every Q-column boundary, [S][nq][H][N]
   // backward outputs

@@ -445,8 +445,9 @@ __device__ __forceinline__ StripId strip_id(const Geo& ge, const Args<T>& a, boo
 
 // ================================================================== forward
 
-template <typename T, int N, int CW, int SH, bool EMIT = false>
+template <typename T, int N, int CW, int SH, bool EMIT = false, bool ACC = false>
 __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel(const Args<T> a) {
+  using F = Fn<T, ACC>;
   using TS = T2Shape<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
   constexpr uint32_t ES = sizeof(T);
@@ -479,9 +480,9 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   const ColVec<T, SV> cv = col_vec<T, N, SV>(j2);
   T A1[SH], A2[SV];
 #pragma unroll
-  for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
+  for (int e = 0; e < SH; ++e) A1[e] = F::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
 #pragma unroll
-  for (int e = 0; e < SV; ++e) A2[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + cv.state(e)]);
+  for (int e = 0; e < SV; ++e) A2[e] = F::a_scale(a.A[static_cast<int64_t>(p) * N + s2 * SV + cv.state(e)]);
 
   for (int e = lane; e < TS::F_TOTAL; e += 32) sm[e] = T(0);
   __syncwarp();
@@ -564,7 +565,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
     // ---- delta = softplus(z + bias) and delta x, once per cell
 #pragma unroll
     for (int c = lane; c < CELLS; c += 32) {
-      const T d = Num<T>::softplus(Ds[c] + bias);
+      const T d = F::softplus(Ds[c] + bias);
       Ds[c] = d;
       DXs[c] = d * Xs[c];
     }
@@ -602,7 +603,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
         for (int jj = 0; jj < 4; ++jj) {
           const int j = j0 + jj;
 #pragma unroll
-          for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
+          for (int e = 0; e < SH; ++e) hh[e] = fma(F::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
           if (j < ncols) sts_vec<T, SH>(hr + j * N, hh);
           // reference CarryState P^h (engine.cpp:188-194): hh at the last column of
           // every reference tile (edge slots stay zero, the reference's pass-through)
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
         T acc0 = T(0), acc1 = T(0);
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
-          hv[e] = fma(Num<T>::exp_scaled(dj * A2[e]), hv[e], h4[e]);
+          hv[e] = fma(F::exp_scaled(dj * A2[e]), hv[e], h4[e]);
           if (e & 1)
             acc1 = fma(c4[e], hv[e], acc1);
           else
@@ -675,8 +676,9 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 
 // CW = 16: up to 13 warps (128 registers); CW = 32 (fp32, N <= 16): up to 8
 // warps with the register room for 32-column strips (7 strips cover 200 columns)
-template <typename T, int N, int CW, int SH>
+template <typename T, int N, int CW, int SH, bool ACC = false>
 __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
+  using F = Fn<T, ACC>;
   using TS = T2Shape<T, N, CW, SH>;
   constexpr int R = TS::R, QH = TS::QH, QV = TS::QV, SV = TS::SV, BP = TS::BP, CELLS = TS::CELLS;
   constexpr int RG = TS::RG;
@@ -711,13 +713,13 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const ColVec<T, SV> cv = col_vec<T, N, SV>(j2);
   T A1[SH];
 #pragma unroll
-  for (int e = 0; e < SH; ++e) A1[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
+  for (int e = 0; e < SH; ++e) A1[e] = F::a_scale(a.A[static_cast<int64_t>(p) * N + q1 * SH + e]);
 
   for (int e = lane; e < TS::B_TOTAL; e += 32) sm[e] = T(0);
   __syncwarp();
   // column lanes re-read their scaled A from shared memory in each phase (registers)
   T* As = sm + TS::B_AS;
-  for (int e = lane; e < N; e += 32) As[e] = Num<T>::a_scale(a.A[static_cast<int64_t>(p) * N + e]);
+  for (int e = lane; e < N; e += 32) As[e] = F::a_scale(a.A[static_cast<int64_t>(p) * N + e]);
   T* DAs = sm + TS::B_DAC + lane * SV;  // this lane's column-lane dA accumulators
   __syncwarp();
 
@@ -841,9 +843,9 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
 #pragma unroll
     for (int c = lane; c < CELLS; c += 32) {
       const T v = Ds[c] + bias;
-      const T d = Num<T>::softplus(v);
+      const T d = F::softplus(v);
       Ds[c] = d;
-      SGs[c] = Num<T>::sigmoid(v);
+      SGs[c] = F::sigmoid(v);
       DXs[c] = d * Xs[c];
     }
     __syncwarp();
@@ -861,7 +863,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
           const T g = fma(g4[e], dyv, dn[e]);
-          dn[e] = Num<T>::exp_scaled(dj * A2[e]) * g;
+          dn[e] = F::exp_scaled(dj * A2[e]) * g;
           g4[e] = g;
         }
         if (col_ok) cv.sts(gcol + r * BP, g4);
@@ -884,7 +886,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
         for (int jj = 0; jj < 4; ++jj) {
           const int j = j0 + jj;
 #pragma unroll
-          for (int e = 0; e < SH; ++e) hh[e] = fma(Num<T>::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
+          for (int e = 0; e < SH; ++e) hh[e] = fma(F::exp_scaled(d4[jj] * A1[e]), hh[e], bc[j][e] * u4[jj]);
           if (j < ncols) sts_vec<T, SH>(hr + j * N, hh);
         }
       }
@@ -909,7 +911,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
         T ddv = T(0);
 #pragma unroll
         for (int e = 0; e < SV; ++e) {
-          const T av = Num<T>::exp_scaled(dj * A2[e]);
+          const T av = F::exp_scaled(dj * A2[e]);
           const T tv = g4[e] * hcur[e] * av;  // G h(i-1,j) Abar
           dAc[e] = fma(tv, dj, dAc[e]);
           ddv = fma(tv, A2[e], ddv);
@@ -975,7 +977,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           T dd = T(0), sg = T(0), dBv[SH];
 #pragma unroll
           for (int e = 0; e < SH; ++e) {
-            const T av = Num<T>::exp_scaled(dj * A1[e]);
+            const T av = F::exp_scaled(dj * A1[e]);
             const T gh = g4[e] + rho[e];  // engine.cpp:346
             rho[e] = av * gh;
             const T th = rho[e] * hl[e];  // Gh hh(i,j-1) Abar

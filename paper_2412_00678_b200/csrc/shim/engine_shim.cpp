@@ -244,7 +244,7 @@ scan2d_desc make_desc(int h, int w, int n, int t) {
   d.params_period = 1;
   d.bc_group = 1;
   d.dtype = sizeof(T) == 8 ? SCAN2D_F64 : SCAN2D_F32;
-  d.reserved = 0;
+  d.flags = std::getenv("SCAN2D_ACCURATE") ? SCAN2D_FLAG_ACCURATE : 0;
   return d;
 }
 

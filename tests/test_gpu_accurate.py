@@ -1,0 +1,58 @@
+"""The accurate-exponential mode (desc flag SCAN2D_FLAG_ACCURATE, -m gpu):
+fp32 results at least as close to the fp64 oracle as the reference's own fp32
+engine (the oracle's fp32 restatement, bit-identical to it), where the default
+MUFU path is ~2-3x further.  Gate on y: accurate <= 1.5 x the
+reference fp32 error (or 2e-7); gradients <= 2 x it (or 3e-7); all <= 1e-4."""
+import numpy as np
+import pytest
+import torch
+
+from oracle_lib import Oracle, rel_error
+from scan_cases import batch_to_torch, make_batch, oracle_bwd, oracle_fwd
+
+CASES = [(4, 200, 200, 16), (16, 56, 56, 1), (32, 16, 16, 16), (4, 60, 90, 8), (2, 64, 64, 32), (3, 14, 14, 4)]
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("S,H,W,N", CASES)
+def test_accurate_mode_matches_reference_fp32_accuracy(orc, S, H, W, N):
+    from paper_2412_00678_b200 import tiled_scan_2d_backward, tiled_scan_2d_forward
+
+    b = make_batch(orc, S, H, W, N, seed0=9000, dtype="f32")
+    (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    ref = oracle_bwd(orc, b, "f64")
+    ref["y"] = oracle_fwd(orc, b, "f64")
+    r32 = oracle_bwd(orc, b, "f32")
+    r32["y"] = oracle_fwd(orc, b, "f32")
+    errs = {}
+    for acc in (False, True):
+        res = tiled_scan_2d_forward(x, z, B, C, A, D, bias, accurate=acc)
+        g = tiled_scan_2d_backward(res.saved, dy)
+        torch.cuda.synchronize()
+        got = dict(y=res.y, dx=g.dx, dz=g.dz_raw, dA=g.da, dB=g.db, dC=g.dc, dD=g.dd, dbias=g.dbias)
+        errs[acc] = {k: rel_error(v.cpu().numpy().reshape(-1), np.asarray(ref[k]).reshape(-1)) for k, v in got.items()}
+    refe = {k: rel_error(np.asarray(r32[k]).reshape(-1), np.asarray(ref[k]).reshape(-1)) for k in errs[True]}
+    acc = errs[True]
+    assert acc["y"] <= max(1.5 * refe["y"], 2e-7), (acc["y"], refe["y"])  # (2e-7: ~2 ulp floor, small cases)
+    for k, v in acc.items():
+        assert v <= 1e-4
+        assert v <= max(2.0 * refe[k], 3e-7), (k, v, refe[k])
+    if N in (4, 8, 16, 32):  # the tile kernels: the accurate mode is strictly closer on y
+        assert acc["y"] < errs[False]["y"]
+
+
+def test_accurate_flag_rejects_unknown_bits():
+    import ctypes as C
+
+    from paper_2412_00678_b200 import _native as nat
+
+    d = nat.make_desc(2, 8, 8, 4)
+    d.flags = 2
+    assert nat.lib.scan2d_check_desc(C.byref(d)) == nat.EINVAL
+    d.flags = nat.FLAG_ACCURATE
+    assert nat.lib.scan2d_check_desc(C.byref(d)) == nat.OK
