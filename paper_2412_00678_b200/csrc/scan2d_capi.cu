@@ -166,6 +166,7 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   // tile kernels: bulk L2 prefetch distance in tiles (1000 = off)
   p.pft_f = env_int("SCAN2D_TILE_PFF", 1000);
   p.pft_b = env_int("SCAN2D_TILE_PFB", 1);  // measured on cfg2: 1 tile ahead 0.308 vs 0.326 ms
+  p.pf_mode = env_int("SCAN2D_TILE_PFMODE", 2);
   if (p.pft_f >= 1000) p.pft_f = 0;
   if (p.pft_b >= 1000) p.pft_b = 0;
   // small problems (inputs well inside L2): the tile kernels prefetch every

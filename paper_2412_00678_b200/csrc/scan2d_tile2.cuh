@@ -307,28 +307,46 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Rows r0 .. r0+R-1 of the strip, one row per lane: the B / C spans (ncols x N
-// elements each) and the per-cell planes (x, z and, backward, dy) prefetched
-// into L2 by the TMA unit, so the tile's register / cp.async loads hit L2.
+// L2 prefetch of rows r0 .. r0+R-1 of the strip (B / C spans of ncols x N
+// elements, and the x / z / dy cells), so the tile's register / cp.async loads
+// hit L2.  Mode 1: per-lane prefetch.global.L2 of 128-byte lines (three
+// instructions per lane per tile); mode 2: bulk prefetches by the TMA unit
+// (cp.async.bulk.prefetch.L2), one per row span, issued by lane 0.  (A bulk
+// prefetch takes its address in a uniform register: issued from many lanes
+// with different addresses the compiler serialises them in a loop over lanes,
+// measured as ~9 % of the backward's issue slots.)
 template <typename T, int R>
-__device__ __forceinline__ void prefetch_tile_l2(int lane, int r0, int H, int ncols, int N, size_t WN, int W,
-                                                 const T* Bs, const T* Cs, const T* xs, const T* zs,
+__device__ __forceinline__ void prefetch_tile_l2(int mode, int lane, int r0, int H, int ncols, int N, size_t WN,
+                                                 int W, const T* Bs, const T* Cs, const T* xs, const T* zs,
                                                  const T* ys, bool xvec) {
-  // the per-cell planes only when their rows are 16-byte aligned (bulk copies need it)
-  const int planes = !xvec ? 2 : ys != nullptr ? 5 : 4;
-  if (lane < planes * R) {
-    const int r = r0 + lane % R, k = lane / R;
-    if (r < H) {
-      const uint32_t sb = static_cast<uint32_t>(ncols * N * sizeof(T));
-      const uint32_t sx = static_cast<uint32_t>(ncols * sizeof(T));
-      const T* p = k == 0 ? Bs + static_cast<size_t>(r) * WN
-                 : k == 1 ? Cs + static_cast<size_t>(r) * WN
-                 : k == 2 ? xs + static_cast<size_t>(r) * W
-                 : k == 3 ? zs + static_cast<size_t>(r) * W
-                          : ys + static_cast<size_t>(r) * W;
-      bulk_prefetch_l2(p, k < 2 ? sb : sx);
+  const int rows = min(R, H - r0);
+  if (rows <= 0) return;
+  const uint32_t sb = static_cast<uint32_t>(ncols * N * sizeof(T));
+  if (mode == 2) {
+    if (lane == 0) {
+      for (int r = 0; r < rows; ++r) {
+        bulk_prefetch_l2(Bs + static_cast<size_t>(r0 + r) * WN, sb);
+        bulk_prefetch_l2(Cs + static_cast<size_t>(r0 + r) * WN, sb);
+      }
     }
+    return;
   }
+  // mode 1: lines of the B / C row spans (<= 2 * R * 8 lines of 128 B for a
+  // 1 KB span), then one line per x / z / dy row
+  const int lines = static_cast<int>((sb + 127) / 128);
+  const int total = 2 * rows * lines;
+  for (int u = lane; u < total; u += 32) {
+    const int plane = u / (rows * lines), rem = u % (rows * lines), r = rem / lines, l = rem % lines;
+    const char* base = reinterpret_cast<const char*>((plane == 0 ? Bs : Cs) + static_cast<size_t>(r0 + r) * WN);
+    prefetch_l2(base + l * 128);
+  }
+  const int planes = ys != nullptr ? 3 : 2;
+  if (lane < planes * rows) {
+    const int k = lane / rows, r = lane % rows;
+    const T* p = (k == 0 ? xs : k == 1 ? zs : ys) + static_cast<size_t>(r0 + r) * W;
+    prefetch_l2(p);
+  }
+  (void)xvec;
 }
 
 
@@ -527,16 +545,17 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   load_b_rows<T, CW, SH>(bc, Bg, r1, H, WN, ncols, N);
 
   const int pft = a.plan.pf_all ? 0 : a.plan.pft_f;
+  const int pfmode = a.plan.pf_mode;
   if (a.plan.pf_all)
     for (int t2 = 1; t2 < ntiles; ++t2)
-      prefetch_tile_l2<T, R>(lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr, xrow16);
+      prefetch_tile_l2<T, R>(pfmode, lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr, xrow16);
   for (int t = 0; t < ntiles; ++t) {
     const int r0 = t * R;
     const int par = t & 1;
     const int sh = slot_next(sc), sn = slot_next(sh);
 #ifndef S2D_NO_PF
     if (pft > 0 && t + pft < ntiles)
-      prefetch_tile_l2<T, R>(lane, r0 + pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr, xrow16);
+      prefetch_tile_l2<T, R>(pfmode, lane, r0 + pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, nullptr, xrow16);
 #endif
     // ---- prefetch tile t+1: C into the free slot, x / z into the other parity
     //      (its B operand is loaded into the same registers right after phase 1)
@@ -782,15 +801,16 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   }
 
   const int pft = a.plan.pf_all ? 0 : a.plan.pft_b;
+  const int pfmode = a.plan.pf_mode;
   if (a.plan.pf_all)
     for (int t2 = ntiles - 2; t2 >= 0; --t2)
-      prefetch_tile_l2<T, R>(lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
+      prefetch_tile_l2<T, R>(pfmode, lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
   for (int t = ntiles - 1; t >= 0; --t) {
     const int u = ntiles - 1 - t;  // visiting index (ring phase)
     const int r0 = t * R;
 #ifndef S2D_NO_PF
     if (pft > 0 && t - pft >= 0)
-      prefetch_tile_l2<T, R>(lane, r0 - pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
+      prefetch_tile_l2<T, R>(pfmode, lane, r0 - pft * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
 #endif
     const int rows = min(R, H - r0);
     const int par = t & 1;
