@@ -21,6 +21,6 @@ for k in bwd fwd; do
 done
 for t in memcheck racecheck synccheck; do
   echo "== $t" >> gpurun_out/r02_sanitizers.txt
-  timeout 900 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize.py 2>&1 | tail -6 >> gpurun_out/r02_sanitizers.txt
+  timeout 900 compute-sanitizer --tool $t --print-limit 20 $( [ $t = synccheck ] && echo --num-cuda-barriers 8192 ) python tools/sanitize.py 2>&1 | tail -6 >> gpurun_out/r02_sanitizers.txt
 done
 tail -20 gpurun_out/r02_sanitizers.txt
