@@ -123,125 +123,171 @@ __global__ void flat_readout_kernel(const T* __restrict__ x, const T* __restrict
 
 // flat1d, parallel (the "CUB 1D scan" of Table 3 / Mamba's selective scan;
 // block_scan_1d_forward's segmented block scan, block_scan.cpp:28-88, on the
-// GPU): one CTA per scan walks the row-major flattened grid in chunks of
-// kThreads x kEpt elements.  Per chunk and state d: the affine pairs
-// (Abar, Bbar x) of a thread's kEpt elements are folded in registers, the
-// kThreads folds are combined by a warp shuffle scan and a scan over the warp
-// totals in shared memory, the running carry of the previous chunks enters as
-// the head of the sequence (b <- fma(a, carry, b), block_scan.cpp:51), and
-// y accumulates C_d h over d ascending in registers (engine.cpp:506-518) --
-// the N state sequences never touch HBM.  B and C of the chunk are staged in
-// shared memory with coalesced loads.
+// GPU) with a decoupled look-back across CTAs.  The row-major flattening of
+// every scan is cut into chunks of kFlatThreads x kFlatEpt elements; CTAs
+// take chunk tickets in order (a chunk's predecessors were handed out first).
+// Per chunk and state d: the affine pairs (Abar, Bbar x) of a thread's
+// elements are folded in registers, combined by a warp shuffle scan and a
+// scan over the warp totals; the CTA publishes the chunk AGGREGATE, then
+// looks back over its predecessors -- composing aggregates until it meets a
+// published INCLUSIVE state -- to get the state entering the chunk
+// (block_scan.cpp:51: the carry folded into the head), publishes its own
+// INCLUSIVE state and finishes y = sum_d C_d h_d (d ascending, engine.cpp:
+// 506-518) in registers.  The N state sequences never touch HBM; only
+// 3 N values per chunk do.
 constexpr int kFlatThreads = 256;
 constexpr int kFlatEpt = 2;
 constexpr int kFlatMaxN = 16;  // larger N: the sequential flat kernels above
+constexpr int kFlatChunk = kFlatThreads * kFlatEpt;
+
+struct FlatWs {  // workspace: [ticket][status S*nch][aggA, aggB, inc: S*nch*N each]
+  int* ticket;
+  int* status;  // 0 none, 1 aggregate, 2 inclusive
+  void* vals;
+};
 
 template <typename T, int N>
-__global__ void __launch_bounds__(kFlatThreads) flat_block_kernel(
+__global__ void __launch_bounds__(kFlatThreads) flat_lookback_kernel(
     const T* __restrict__ x, const T* __restrict__ z, const T* __restrict__ B, const T* __restrict__ C,
-    const T* __restrict__ A, const T* __restrict__ Dskip, const T* __restrict__ bias, int64_t L, int P, int G,
-    T* __restrict__ y) {
-  constexpr int CH = kFlatThreads * kFlatEpt;
+    const T* __restrict__ A, const T* __restrict__ Dskip, const T* __restrict__ bias, int64_t S, int64_t L,
+    int nch, int P, int G, T* __restrict__ y, FlatWs ws) {
   constexpr int NW = kFlatThreads / 32;
-  extern __shared__ __align__(16) unsigned char flat_smem[];
-  T* sB = reinterpret_cast<T*>(flat_smem);          // [CH][N]
-  T* sC = sB + CH * N;                              // [CH][N]
-  T* wa = sC + CH * N;                              // [NW][N] warp totals (a)
-  T* wb = wa + NW * kFlatMaxN;                      // [NW][N] warp totals (b)
-  T* carry = wb + NW * kFlatMaxN;                   // [N] running h
-  const int64_t s = blockIdx.x;
-  const int64_t p = s % P, g = s / G;
+  __shared__ T wa[NW][N], wb[NW][N], carry[N], aggA[N], aggB[N];
+  __shared__ int64_t tile_s;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) tile_s = atomicAdd(ws.ticket, 1);
+  __syncthreads();
+  const int64_t tile = tile_s;
+  const int64_t s = tile / nch;
+  const int c = static_cast<int>(tile % nch);
+  const int64_t p = s % P, g = s / G;
+  const int64_t base = static_cast<int64_t>(c) * kFlatChunk;
+  const int cnt = static_cast<int>(L - base < kFlatChunk ? L - base : kFlatChunk);
   const T bs = bias[p], dsk = Dskip[p];
-  for (int d = tid; d < N; d += kFlatThreads) carry[d] = T(0);
-  const T* xs = x + s * L;
-  const T* zs = z + s * L;
-  const T* Bs = B + g * L * N;
-  const T* Cs = C + g * L * N;
-  for (int64_t base = 0; base < L; base += CH) {
-    const int cnt = static_cast<int>(L - base < CH ? L - base : CH);
-    __syncthreads();  // previous chunk done with sB / sC / carry reads
-    for (int e = tid; e < cnt * N; e += kFlatThreads) {
-      sB[e] = Bs[base * N + e];
-      sC[e] = Cs[base * N + e];
-    }
-    T dl[kFlatEpt], xv[kFlatEpt], yacc[kFlatEpt];
+  const size_t nv = static_cast<size_t>(S) * nch * N;
+  T* vA = static_cast<T*>(ws.vals);
+  T* vB = vA + nv;
+  T* vI = vB + nv;
+  const size_t slot = (static_cast<size_t>(s) * nch + c) * N;
+
+  T dl[kFlatEpt], xv[kFlatEpt], yacc[kFlatEpt], bq[kFlatEpt][N], cq[kFlatEpt][N];
 #pragma unroll
-    for (int k = 0; k < kFlatEpt; ++k) {
-      const int idx = tid * kFlatEpt + k;
-      const bool ok = idx < cnt;
-      xv[k] = ok ? xs[base + idx] : T(0);
-      dl[k] = ok ? Num<T>::softplus(zs[base + idx] + bs) : T(0);
-      yacc[k] = T(0);
-    }
-    __syncthreads();
-    T fa[N], fb[N];  // this thread's exclusive prefix within its warp
+  for (int k = 0; k < kFlatEpt; ++k) {
+    const int idx = tid * kFlatEpt + k;
+    const bool ok = idx < cnt;
+    const int64_t e = base + (ok ? idx : 0);
+    xv[k] = ok ? x[s * L + e] : T(0);
+    dl[k] = ok ? Num<T>::softplus(z[s * L + e] + bs) : T(0);
+    yacc[k] = T(0);
 #pragma unroll
     for (int d = 0; d < N; ++d) {
-      const T ad = Num<T>::a_scale(A[p * N + d]);
-      T aa = T(1), bb = T(0);
-#pragma unroll
-      for (int k = 0; k < kFlatEpt; ++k) {
-        const int idx = tid * kFlatEpt + k;
-        const bool ok = idx < cnt;
-        const T av = ok ? Num<T>::exp_scaled(dl[k] * ad) : T(1);
-        const T bx = ok ? (dl[k] * sB[idx * N + d]) * xv[k] : T(0);
-        bb = fma(av, bb, bx);
-        aa = av * aa;
-      }
-      // inclusive warp scan of the folds (compose: earlier first)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const T pa = __shfl_up_sync(kFull, aa, o), pb = __shfl_up_sync(kFull, bb, o);
-        if (lane >= o) {
-          bb = fma(aa, pb, bb);
-          aa = aa * pa;
-        }
-      }
-      if (lane == 31) {
-        wa[wid * kFlatMaxN + d] = aa;
-        wb[wid * kFlatMaxN + d] = bb;
-      }
-      // exclusive within the warp
-      const T ea = __shfl_up_sync(kFull, aa, 1), eb = __shfl_up_sync(kFull, bb, 1);
-      fa[d] = lane == 0 ? T(1) : ea;
-      fb[d] = lane == 0 ? T(0) : eb;
+      bq[k][d] = ok ? B[(g * L + e) * N + d] : T(0);
+      cq[k][d] = ok ? C[(g * L + e) * N + d] : T(0);
     }
-    __syncthreads();
+  }
+  T fa[N], fb[N];  // this thread's exclusive prefix within its warp
 #pragma unroll
-    for (int d = 0; d < N; ++d) {
-      // prefix = carry, then the totals of the warps before this one, then the lane prefix
-      T h = carry[d];
-      for (int w = 0; w < wid; ++w) h = fma(wa[w * kFlatMaxN + d], h, wb[w * kFlatMaxN + d]);
-      h = fma(fa[d], h, fb[d]);
-      const T ad = Num<T>::a_scale(A[p * N + d]);
-#pragma unroll
-      for (int k = 0; k < kFlatEpt; ++k) {
-        const int idx = tid * kFlatEpt + k;
-        if (idx < cnt) {
-          const T av = Num<T>::exp_scaled(dl[k] * ad);
-          h = fma(av, h, (dl[k] * sB[idx * N + d]) * xv[k]);
-          yacc[k] = fma(sC[idx * N + d], h, yacc[k]);
-        }
-      }
-      if (tid * kFlatEpt + kFlatEpt - 1 >= cnt - 1 && tid * kFlatEpt <= cnt - 1) fb[d] = h;  // chunk's last h
-    }
+  for (int d = 0; d < N; ++d) {
+    const T ad = Num<T>::a_scale(A[p * N + d]);
+    T aa = T(1), bb = T(0);
 #pragma unroll
     for (int k = 0; k < kFlatEpt; ++k) {
-      const int idx = tid * kFlatEpt + k;
-      if (idx < cnt) y[s * L + base + idx] = fma(dsk, xv[k], yacc[k]);
+      const bool ok = tid * kFlatEpt + k < cnt;
+      const T av = ok ? Num<T>::exp_scaled(dl[k] * ad) : T(1);
+      bb = fma(av, bb, (dl[k] * bq[k][d]) * xv[k]);
+      aa = av * aa;
     }
-    __syncthreads();  // every thread has read carry[]
-    if (tid * kFlatEpt + kFlatEpt - 1 >= cnt - 1 && tid * kFlatEpt <= cnt - 1) {
 #pragma unroll
-      for (int d = 0; d < N; ++d) carry[d] = fb[d];
+    for (int o = 1; o < 32; o <<= 1) {
+      const T pa = __shfl_up_sync(kFull, aa, o), pb = __shfl_up_sync(kFull, bb, o);
+      if (lane >= o) {
+        bb = fma(aa, pb, bb);
+        aa = aa * pa;
+      }
     }
+    if (lane == 31) wa[wid][d] = aa, wb[wid][d] = bb;
+    const T ea = __shfl_up_sync(kFull, aa, 1), eb = __shfl_up_sync(kFull, bb, 1);
+    fa[d] = lane == 0 ? T(1) : ea;
+    fb[d] = lane == 0 ? T(0) : eb;
+  }
+  __syncthreads();
+  // chunk aggregate per state, then publish it (AGGREGATE) or, for the first
+  // chunk of a scan, the inclusive state directly
+  if (tid < N) {
+    T a2 = T(1), b2 = T(0);
+    for (int w = 0; w < NW; ++w) {
+      b2 = fma(wa[w][tid], b2, wb[w][tid]);
+      a2 = wa[w][tid] * a2;
+    }
+    aggA[tid] = a2, aggB[tid] = b2;
+    if (c == 0) {
+      vI[slot + tid] = b2;
+    } else {
+      vA[slot + tid] = a2;
+      vB[slot + tid] = b2;
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0)
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ws.status + s * nch + c), "r"(c == 0 ? 2 : 1)
+                 : "memory");
+  // look back (one thread per state)
+  if (tid < N) {
+    T h = T(0);
+    if (c > 0) {
+      T accA = T(1), accB = T(0);
+      int k = c - 1;
+      while (true) {
+        int st;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(st) : "l"(ws.status + s * nch + k) : "memory");
+        if (st == 2) {
+          h = fma(accA, __ldcg(vI + (static_cast<size_t>(s) * nch + k) * N + tid), accB);
+          break;
+        }
+        if (st == 1) {
+          const size_t o = (static_cast<size_t>(s) * nch + k) * N + tid;
+          accB = fma(accA, __ldcg(vB + o), accB);
+          accA = accA * __ldcg(vA + o);
+          if (--k < 0) {
+            h = accB;
+            break;
+          }
+        }
+      }
+      vI[slot + tid] = fma(aggA[tid], h, aggB[tid]);
+      __threadfence();
+    }
+    carry[tid] = h;
+  }
+  __syncthreads();
+  if (tid == 0 && c > 0)
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ws.status + s * nch + c), "r"(2) : "memory");
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    T h = carry[d];
+    for (int w = 0; w < wid; ++w) h = fma(wa[w][d], h, wb[w][d]);
+    h = fma(fa[d], h, fb[d]);
+    const T ad = Num<T>::a_scale(A[p * N + d]);
+#pragma unroll
+    for (int k = 0; k < kFlatEpt; ++k) {
+      if (tid * kFlatEpt + k < cnt) {
+        h = fma(Num<T>::exp_scaled(dl[k] * ad), h, (dl[k] * bq[k][d]) * xv[k]);
+        yacc[k] = fma(cq[k][d], h, yacc[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kFlatEpt; ++k) {
+    const int idx = tid * kFlatEpt + k;
+    if (idx < cnt) y[s * L + base + idx] = fma(dsk, xv[k], yacc[k]);
   }
 }
 
-size_t flat_block_smem(int N, size_t es) {
-  return es * (2 * static_cast<size_t>(kFlatThreads) * kFlatEpt * N + 2 * (kFlatThreads / 32) * kFlatMaxN +
-               kFlatMaxN);
+size_t flat_lookback_ws(int64_t S, int64_t L, int N, size_t es) {
+  const int64_t nch = (L + kFlatChunk - 1) / kFlatChunk;
+  return 256 + (static_cast<size_t>(S * nch) * sizeof(int) + 255) / 256 * 256 +
+         3 * static_cast<size_t>(S * nch) * N * es;
 }
 
 unsigned blocks_for(int64_t n, int threads) { return static_cast<unsigned>((n + threads - 1) / threads); }
@@ -270,27 +316,28 @@ int run_flat(const scan2d_desc& d, const void* x, const void* z, const void* B, 
   const int64_t S = d.num_scans;
   const int64_t L = static_cast<int64_t>(d.height) * d.width;
   if (d.state_dim <= kFlatMaxN && (d.state_dim & (d.state_dim - 1)) == 0) {
-    const size_t smem = flat_block_smem(d.state_dim, sizeof(T));
-    const unsigned grid = static_cast<unsigned>(S);
-    cudaError_t e = cudaSuccess;
+    const int64_t nch = (L + kFlatChunk - 1) / kFlatChunk;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    FlatWs fw{reinterpret_cast<int*>(w), reinterpret_cast<int*>(w + 256),
+              w + 256 + (static_cast<size_t>(S * nch) * sizeof(int) + 255) / 256 * 256};
+    // ticket + chunk status flags start at zero on every call
+    if (cudaMemsetAsync(w, 0, 256 + static_cast<size_t>(S * nch) * sizeof(int), st) != cudaSuccess)
+      return SCAN2D_ECUDA;
+    const unsigned grid = static_cast<unsigned>(S * nch);
     auto go = [&](auto kern) {
-      if (smem > 48 * 1024)
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (e == cudaSuccess)
-        kern<<<grid, kFlatThreads, smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(z),
-                                               static_cast<const T*>(B), static_cast<const T*>(C),
-                                               static_cast<const T*>(A), static_cast<const T*>(Dskip),
-                                               static_cast<const T*>(bias), L, d.params_period, d.bc_group,
-                                               static_cast<T*>(y));
+      kern<<<grid, kFlatThreads, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(z),
+                                          static_cast<const T*>(B), static_cast<const T*>(C),
+                                          static_cast<const T*>(A), static_cast<const T*>(Dskip),
+                                          static_cast<const T*>(bias), S, L, static_cast<int>(nch),
+                                          d.params_period, d.bc_group, static_cast<T*>(y), fw);
     };
     switch (d.state_dim) {
-      case 1: go(flat_block_kernel<T, 1>); break;
-      case 2: go(flat_block_kernel<T, 2>); break;
-      case 4: go(flat_block_kernel<T, 4>); break;
-      case 8: go(flat_block_kernel<T, 8>); break;
-      default: go(flat_block_kernel<T, 16>); break;
+      case 1: go(flat_lookback_kernel<T, 1>); break;
+      case 2: go(flat_lookback_kernel<T, 2>); break;
+      case 4: go(flat_lookback_kernel<T, 4>); break;
+      case 8: go(flat_lookback_kernel<T, 8>); break;
+      default: go(flat_lookback_kernel<T, 16>); break;
     }
-    if (e != cudaSuccess) return SCAN2D_ECUDA;
     return cudaGetLastError() == cudaSuccess ? SCAN2D_OK : SCAN2D_ECUDA;
   }
   T* hs = static_cast<T*>(ws);
@@ -322,8 +369,8 @@ size_t scan2d_comparator_workspace_bytes(const scan2d_desc* d, int variant) {
   const size_t es = d->dtype == SCAN2D_F64 ? 8 : 4;
   const size_t S = static_cast<size_t>(d->num_scans), HW = static_cast<size_t>(d->height) * d->width;
   if (variant == SCAN2D_VARIANT_NAIVE) return es * S * d->state_dim * (HW + d->width);
-  if (d->state_dim <= s2d::kFlatMaxN && (d->state_dim & (d->state_dim - 1)) == 0)
-    return 16;  // block-scan kernel: no HBM state sequences
+  if (d->state_dim <= s2d::kFlatMaxN && (d->state_dim & (d->state_dim - 1)) == 0)  // look-back kernel
+    return s2d::flat_lookback_ws(d->num_scans, static_cast<int64_t>(d->height) * d->width, d->state_dim, es);
   return es * S * HW * d->state_dim;
 }
 
