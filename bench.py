@@ -45,6 +45,10 @@ WORKLOADS = {
     "cfg4c": dict(S=64 * 384, H=14, W=14, N=1, bwd=True, desc="VMamba sweep: B=64 D=384 N=1 14x14 fwd+bwd (configs[3])"),
     "cfg4d": dict(S=64 * 768, H=7, W=7, N=1, bwd=True, desc="VMamba sweep: B=64 D=768 N=1 7x7 fwd+bwd (configs[3])"),
     "cfg5": dict(S=256, H=1024, W=1024, N=16, bwd=False, desc="giga-pixel: B=1 D=256 N=16 1024x1024 fwd (configs[4])"),
+    # the 2DMamba block layout of cfg2 (model.cpp:150-193): B / C shared by the D = 128 channels of the
+    # batch item (G = 128), A / D / bias per channel -- SURVEY.md §8f row 2
+    "cfg2m": dict(S=128, H=200, W=200, N=16, G=128, bwd=True,
+                  desc="WSI MIL model layout: B=1 D=128 N=16 200x200, B/C shared by the 128 channels, fwd+bwd"),
 }
 
 # How `--gpus N` scales each workload (ShardedScan2d: contiguous scan ranges,
@@ -52,7 +56,7 @@ WORKLOADS = {
 # single-GPU batch (N slides / images -- per-GPU work fixed); "strong": the
 # BASELINE batch itself is split over the N GPUs (configs[3], "batch-sharded
 # over 2/4/8 GPUs").
-SCALING = {"cfg1": "weak", "cfg2": "weak", "cfg5": "weak", "cfg3": "strong", "cfg4a": "strong",
+SCALING = {"cfg1": "weak", "cfg2": "weak", "cfg2m": "weak", "cfg5": "weak", "cfg3": "strong", "cfg4a": "strong",
            "cfg4b": "strong", "cfg4c": "strong", "cfg4d": "strong"}
 
 L2_BYTES = 126 * 1024 * 1024
@@ -66,9 +70,12 @@ NVML_REASONS = {
 def alg_bytes(wl, es=4):
     """Reference counting model (memsim.cpp:45-46): per scan
     fwd = es*H*W*(3+2N) (x, z, B, C in; y out), bwd = es*H*W*(5+4N)
-    (x, z, dy, B, C in; dx, dz, dB, dC out)."""
+    (x, z, dy, B, C in; dx, dz, dB, dC out).  With B / C shared by groups of G
+    scans (the model layout) the B / C / dB / dC terms count once per group:
+    fwd = es*H*W*(3S + 2N S/G), bwd = es*H*W*(5S + 4N S/G)."""
     hw = wl["H"] * wl["W"]
-    return wl["S"] * es * hw * (3 + 2 * wl["N"]), wl["S"] * es * hw * (5 + 4 * wl["N"])
+    S, N, G = wl["S"], wl["N"], wl.get("G", 1)
+    return es * hw * (3 * S + 2 * N * S // G), es * hw * (5 * S + 4 * N * S // G)
 
 
 def measured_peak():
@@ -156,7 +163,8 @@ def synth_inputs(torch, wl, dev, seed, dtype):
     r = lambda *s: torch.randn(*s, generator=g, device=dev, dtype=dtype)
     u = lambda *s: torch.rand(*s, generator=g, device=dev, dtype=dtype)
     x, z = r(S, H, W), r(S, H, W)
-    B, C = r(S, H, W, N), r(S, H, W, N)
+    G = wl.get("G", 1)
+    B, C = r(S // G, H, W, N), r(S // G, H, W, N)
     A = -(0.05 + 0.9 * u(S, N))
     D = r(S)
     bias = u(S) - 0.5
@@ -374,8 +382,8 @@ def main():
     from paper_2412_00678_b200.launcher import ShardedScan2d
 
     dtype = torch.float32
-    sharded = ShardedScan2d(S_global, wl["H"], wl["W"], wl["N"], rank, world, dist=dist, tile=16, dtype=dtype,
-                            device=dev, with_backward=wl["bwd"])
+    sharded = ShardedScan2d(S_global, wl["H"], wl["W"], wl["N"], rank, world, dist=dist,
+                            bc_group=wl.get("G", 1), tile=16, dtype=dtype, device=dev, with_backward=wl["bwd"])
     shard = sharded.shard
     wl_local = dict(wl, S=shard.count)  # this rank's contiguous scan range of the global batch
     assert [sh.count for sh in sharded.shards] == per_gpu
@@ -469,7 +477,7 @@ def main():
     # the reference fp32 engine's) on the same inputs, for its cost
     if not args.no_accurate:
         aop = Scan2dOp(shard.count, wl["H"], wl["W"], wl["N"], tile=16, dtype=dtype, device=dev,
-                       with_backward=wl["bwd"], accurate=True)
+                       with_backward=wl["bwd"], accurate=True, bc_group=wl.get("G", 1))
         aop.check = False
         for _ in range(3):
             aop.forward(*ins, save=wl["bwd"])
@@ -500,7 +508,10 @@ def main():
     #      reference call's contract -- host data in, host results out -- with the
     #      copies pipelined against the kernels inside the library)
     e2e = None
-    if not args.no_e2e:
+    if wl.get("G", 1) > 1:  # scan2d_train_host serves the reference operator contract (per-scan B / C)
+        e2e = {"value": None, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "host-operand path serves per-scan B/C only (scan2d_train_host)"}
+    if not args.no_e2e and e2e is None:
         from paper_2412_00678_b200.api import train_host
 
         hin = [t.cpu().pin_memory() for t in ins]
