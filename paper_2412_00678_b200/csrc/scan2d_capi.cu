@@ -167,6 +167,11 @@ int make_plan(const scan2d_desc& d, Plan& p) {
   p.pft_f = env_int("SCAN2D_TILE_PFF", 1000);
   p.pft_b = env_int("SCAN2D_TILE_PFB", 1);  // measured on cfg2: 1 tile ahead 0.308 vs 0.326 ms
   p.pf_mode = env_int("SCAN2D_TILE_PFMODE", 2);
+  // tile staging: 3 (default) cp.async; 1: C rows by TMA bulk copies, 2: C + x / z / dy rows.  Measured on
+  // cfg2 (fwd / bwd us): cp.async 160 / 304, TMA C 166 / 322, TMA all 177 / 319 -- one bulk copy per row
+  // span issued by one lane serialises the issue; kept as an option (profiles/README.md).
+  p.tma = env_int("SCAN2D_TILE_TMA", 3);
+  if (p.tma > 2) p.tma = 0;
   if (p.pft_f >= 1000) p.pft_f = 0;
   if (p.pft_b >= 1000) p.pft_b = 0;
   // small problems (inputs well inside L2): the tile kernels prefetch every

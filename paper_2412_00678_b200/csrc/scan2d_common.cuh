@@ -616,6 +616,7 @@ struct Plan {
   int pft_f, pft_b;  // tile kernels: bulk L2 prefetch distance in tiles (forward / backward; 0 = off)
   int pf_all;        // tile kernels: prefetch the whole strip into L2 at the start (small problems)
   int pf_mode;       // tile kernels: 1 = per-lane line prefetches, 2 = TMA bulk prefetches (lane 0)
+  int tma;           // tile kernels: stage C (and aligned x / z / dy rows) by TMA bulk copies
 };
 
 template <typename T>

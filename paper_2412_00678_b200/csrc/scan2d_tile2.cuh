@@ -71,13 +71,16 @@ struct T2Shape {
   // forward:  slots[3] | X[2] | Z[2] (z, then delta in place) | DX (delta x)
   static constexpr int F_X = 3 * SLOT, F_Z = F_X + 2 * CELLS, F_DX = F_Z + 2 * CELLS;
   static constexpr int F_TOTAL_RAW = F_DX + CELLS;
-  static constexpr int F_TOTAL = (F_TOTAL_RAW + EPV - 1) / EPV * EPV;
+  // two 8-byte mbarriers (the TMA stage barriers of tiles u and u+1) close the region
+  static constexpr int F_BAR = (F_TOTAL_RAW + EPV - 1) / EPV * EPV;
+  static constexpr int F_TOTAL = F_BAR + EPV;
   // backward: slots[3] | X[2] | Z[2] | DY[2] | DX | SG (sigmoid) | DV (column-lane ddelta) | SCR[N]
   static constexpr int B_X = 3 * SLOT, B_Z = B_X + 2 * CELLS, B_Y = B_Z + 2 * CELLS;
   static constexpr int B_DX = B_Y + 2 * CELLS, B_SG = B_DX + CELLS, B_DV = B_SG + CELLS;
   static constexpr int B_SCR = B_DV + CELLS, B_AS = B_SCR + N, B_DAC = B_AS + N;
   // per-warp regions are padded to 16 bytes (cp.async destinations)
-  static constexpr int B_TOTAL = (B_DAC + 32 * SV + EPV - 1) / EPV * EPV;
+  static constexpr int B_BAR = (B_DAC + 32 * SV + EPV - 1) / EPV * EPV;
+  static constexpr int B_TOTAL = B_BAR + EPV;
   static_assert(QH >= 1 && QH <= 32 && R >= 1 && SV >= 1, "tile shape");
   static_assert(CW % EPV == 0 && (CELLS % EPV) == 0, "16-byte copy units");
 };
@@ -384,6 +387,48 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---- TMA staging of a tile (cp.async.bulk, SASS UBLKCP): lane 0 arms the
+// stage's mbarrier with the tile's byte count and issues one bulk copy per row
+// span -- the C rows (ncols x N elements, contiguous) and, when the rows are
+// 16-byte aligned, the x / z (/ dy) rows; the warp waits on the barrier's phase
+// instead of cp.async groups.  The destination slot was last read by generic
+// loads (the previous use ended with __syncwarp), hence the proxy fence.
+__device__ __forceinline__ void mbar_init_tma(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <typename TS, int N, typename T>
+__device__ __forceinline__ void tma_tile(uint32_t bar, uint32_t cdst, const T* Cg, int r0, int H, size_t WN, int W,
+                                         int ncols, bool cells, uint32_t xd, const T* xg, uint32_t zd, const T* zg,
+                                         uint32_t yd, const T* yg) {
+  constexpr uint32_t ES = sizeof(T);
+  const int rows = max(0, min(TS::R, H - r0));
+  const uint32_t cb = static_cast<uint32_t>(ncols * N) * ES, xb = static_cast<uint32_t>(ncols) * ES;
+  const int planes = !cells ? 0 : (yg != nullptr ? 3 : 2);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(bar, static_cast<uint32_t>(rows) * (cb + planes * xb));
+  for (int r = 0; r < rows; ++r) {
+    const size_t gr = static_cast<size_t>(r0 + r);
+    bulk_g2s(cdst + static_cast<uint32_t>(r * TS::BP) * ES, Cg + gr * WN, cb, bar);
+    if (planes > 0) {
+      const uint32_t co = static_cast<uint32_t>(r * (TS::CELLS / TS::R)) * ES;
+      bulk_g2s(xd + co, xg + gr * W, xb, bar);
+      bulk_g2s(zd + co, zg + gr * W, xb, bar);
+      if (planes > 2) bulk_g2s(yd + co, yg + gr * W, xb, bar);
+    }
+  }
+}
+
 // Carry ring of one CTA: data [nw-1][kRing][32 lanes][SH], barriers full / empty
 // [nw-1][kRing].  Boundary b sits between warps b and b+1.
 template <typename T, int SH>
@@ -537,9 +582,29 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 
   const int ntiles = (H + R - 1) / R;
   int sc = 0;  // slot holding this tile's C; sc+1: hh of this tile; sc+2: C of the next tile
-  issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, 0, H, WN, ncols, lane);
-  issue_cells<TS>(sbase + TS::F_X * ES, xg, 0, H, W, ncols, lane, xrow16);
-  issue_cells<TS>(sbase + TS::F_Z * ES, zg, 0, H, W, ncols, lane, xrow16);
+  // TMA staging (stage barriers at the end of the warp's region) or cp.async
+  const bool tma = a.plan.tma != 0;
+  const bool tcells = a.plan.tma == 2 && xrow16;  // x / z / dy rows by TMA too
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(sm + TS::F_BAR);
+  if (tma) {
+    if (lane == 0) {
+      mbar_init_tma(tbar);
+      mbar_init_tma(tbar + 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0)
+      tma_tile<TS, N>(smem_u32(tbar), sbase + sc * TS::SLOT * ES, Cg, 0, H, WN, W, ncols, tcells,
+                      sbase + TS::F_X * ES, xg, sbase + TS::F_Z * ES, zg, 0u, static_cast<const T*>(nullptr));
+    if (!tcells) {
+      issue_cells<TS>(sbase + TS::F_X * ES, xg, 0, H, W, ncols, lane, xrow16);
+      issue_cells<TS>(sbase + TS::F_Z * ES, zg, 0, H, W, ncols, lane, xrow16);
+    }
+  } else {
+    issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, 0, H, WN, ncols, lane);
+    issue_cells<TS>(sbase + TS::F_X * ES, xg, 0, H, W, ncols, lane, xrow16);
+    issue_cells<TS>(sbase + TS::F_Z * ES, zg, 0, H, W, ncols, lane, xrow16);
+  }
   cp_async_commit();
   T bc[CW][SH];
   load_b_rows<T, CW, SH>(bc, Bg, r1, H, WN, ncols, N);
@@ -560,9 +625,20 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
     // ---- prefetch tile t+1: C into the free slot, x / z into the other parity
     //      (its B operand is loaded into the same registers right after phase 1)
     if (t + 1 < ntiles) {
-      issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, r0 + R, H, WN, ncols, lane);
-      issue_cells<TS>(sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg, r0 + R, H, W, ncols, lane, xrow16);
-      issue_cells<TS>(sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, r0 + R, H, W, ncols, lane, xrow16);
+      if (tma) {
+        if (lane == 0)
+          tma_tile<TS, N>(smem_u32(tbar + ((t + 1) & 1)), sbase + sn * TS::SLOT * ES, Cg, r0 + R, H, WN, W, ncols,
+                          tcells, sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg,
+                          sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, 0u, static_cast<const T*>(nullptr));
+        if (!tcells) {
+          issue_cells<TS>(sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg, r0 + R, H, W, ncols, lane, xrow16);
+          issue_cells<TS>(sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, r0 + R, H, W, ncols, lane, xrow16);
+        }
+      } else {
+        issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, r0 + R, H, WN, ncols, lane);
+        issue_cells<TS>(sbase + (TS::F_X + (par ^ 1) * CELLS) * ES, xg, r0 + R, H, W, ncols, lane, xrow16);
+        issue_cells<TS>(sbase + (TS::F_Z + (par ^ 1) * CELLS) * ES, zg, r0 + R, H, W, ncols, lane, xrow16);
+      }
     }
     cp_async_commit();
     const int i1 = r0 + r1;
@@ -574,6 +650,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
                        *reinterpret_cast<CarryPre<float, SH>*>(&cpre));
     }
     cp_async_wait<1>();
+    if (tma) mbar_wait(tbar + (t & 1), (t >> 1) & 1);
     __syncwarp();
     T* Xs = sm + TS::F_X + par * CELLS;
     T* Ds = sm + TS::F_Z + par * CELLS;  // z, then delta in place
@@ -781,13 +858,34 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
 
   const int ntiles = (H + R - 1) / R;
   int sc = 0;  // slot with C (then G) of this tile; sc+1: hh; sc+2: C of the next tile up
+  const bool tma = a.plan.tma != 0;
+  const bool tcells = a.plan.tma == 2 && xrow16;  // x / z / dy rows by TMA too
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(sm + TS::B_BAR);
   {
     const int rl = (ntiles - 1) * R;
     const int par = (ntiles - 1) & 1;
-    issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, rl, H, WN, ncols, lane);
-    issue_cells<TS>(sbase + (TS::B_X + par * CELLS) * ES, xg, rl, H, W, ncols, lane, xrow16);
-    issue_cells<TS>(sbase + (TS::B_Z + par * CELLS) * ES, zg, rl, H, W, ncols, lane, xrow16);
-    issue_cells<TS>(sbase + (TS::B_Y + par * CELLS) * ES, yg, rl, H, W, ncols, lane, xrow16);
+    if (tma) {
+      if (lane == 0) {
+        mbar_init_tma(tbar);
+        mbar_init_tma(tbar + 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncwarp();
+      if (lane == 0)
+        tma_tile<TS, N>(smem_u32(tbar), sbase + sc * TS::SLOT * ES, Cg, rl, H, WN, W, ncols, tcells,
+                        sbase + (TS::B_X + par * CELLS) * ES, xg, sbase + (TS::B_Z + par * CELLS) * ES, zg,
+                        sbase + (TS::B_Y + par * CELLS) * ES, yg);
+      if (!tcells) {
+        issue_cells<TS>(sbase + (TS::B_X + par * CELLS) * ES, xg, rl, H, W, ncols, lane, xrow16);
+        issue_cells<TS>(sbase + (TS::B_Z + par * CELLS) * ES, zg, rl, H, W, ncols, lane, xrow16);
+        issue_cells<TS>(sbase + (TS::B_Y + par * CELLS) * ES, yg, rl, H, W, ncols, lane, xrow16);
+      }
+    } else {
+      issue_slot<TS, N>(sbase + sc * TS::SLOT * ES, Cg, rl, H, WN, ncols, lane);
+      issue_cells<TS>(sbase + (TS::B_X + par * CELLS) * ES, xg, rl, H, W, ncols, lane, xrow16);
+      issue_cells<TS>(sbase + (TS::B_Z + par * CELLS) * ES, zg, rl, H, W, ncols, lane, xrow16);
+      issue_cells<TS>(sbase + (TS::B_Y + par * CELLS) * ES, yg, rl, H, W, ncols, lane, xrow16);
+    }
     cp_async_commit();
   }
   T bc[CW][SH];
@@ -819,10 +917,23 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
     // previous tile's R2 finished with each column (one register set only)
     if (t > 0) {
       const int ru = r0 - R;
-      issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
-      issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane, xrow16);
-      issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane, xrow16);
-      issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane, xrow16);
+      if (tma) {
+        if (lane == 0)
+          tma_tile<TS, N>(smem_u32(tbar + ((u + 1) & 1)), sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, W, ncols,
+                          tcells, sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg,
+                          sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES,
+                          yg);
+        if (!tcells) {
+          issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane, xrow16);
+          issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane, xrow16);
+          issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane, xrow16);
+        }
+      } else {
+        issue_slot<TS, N>(sbase + sn * TS::SLOT * ES, Cg, ru, H, WN, ncols, lane);
+        issue_cells<TS>(sbase + (TS::B_X + (par ^ 1) * CELLS) * ES, xg, ru, H, W, ncols, lane, xrow16);
+        issue_cells<TS>(sbase + (TS::B_Z + (par ^ 1) * CELLS) * ES, zg, ru, H, W, ncols, lane, xrow16);
+        issue_cells<TS>(sbase + (TS::B_Y + (par ^ 1) * CELLS) * ES, yg, ru, H, W, ncols, lane, xrow16);
+      }
     }
     cp_async_commit();
     const int i1 = r0 + r1;
@@ -849,6 +960,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
       cv.ldg(hp0, a.vtop + (s * W + jg2) * N + s2 * SV);
     }
     cp_async_wait<1>();
+    if (tma) mbar_wait(tbar + (u & 1), (u >> 1) & 1);
     __syncwarp();
     T* Xs = sm + TS::B_X + par * CELLS;
     T* Ds = sm + TS::B_Z + par * CELLS;  // z, then delta in place
