@@ -338,18 +338,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     scaling = args.scaling or SCALING[args.workload]
-    S_global = wl["S"] * world if scaling == "weak" else wl["S"]
-    # largest per-GPU shard (launcher.shard_range with quantum 1: per-scan
-    # parameters and B/C), computed here so the reference arm imports nothing
-    # of the package (no repo .so loaded on its path)
-    base, extra = divmod(S_global, world)
-    per_gpu = [base + (1 if r < extra else 0) for r in range(world)]
-    fb0, _ = alg_bytes(dict(wl, S=max(per_gpu)))
-    config = {"workload": args.workload, "desc": wl["desc"], "S_global": S_global, "S_per_gpu": per_gpu, "H": wl["H"], "W": wl["W"],
-              "N": wl["N"], "tile": 16, "pass": "fwd+bwd" if wl["bwd"] else "fwd",
-              "parallelism": (f"batch-sharded x{world} ({scaling} scaling: contiguous scan ranges per GPU, "
-                              "no collective on the data path)"),
-              "l2": l2_policy(fb0)}
+    config, S_global, per_gpu = build_config(args.workload, world, scaling)
 
     if args.rowband and args.impl == "ours":
         return rowband_main(args, wl, rank, world, local, config)
@@ -663,6 +652,29 @@ def shim_main(args):
                               "d2h_bytes_per_step": out["d2h_bytes_per_pass"]},
                       "detail": out}), flush=True)
     return 0
+
+
+def build_config(workload, world, scaling):
+    """The `config` dict of a bench line -- computed from the workload alone, so
+    both arms (ours and `--impl reference`) print the identical dict."""
+    wl = WORKLOADS[workload]
+    S_global = wl["S"] * world if scaling == "weak" else wl["S"]
+    # largest per-GPU shard (launcher.shard_range with the layout quantum),
+    # computed here so the reference arm imports nothing of the package (no repo
+    # .so loaded on its path)
+    q = wl.get("G", 1)
+    units = S_global // q
+    base, extra = divmod(units, world)
+    per_gpu = [(base + (1 if r < extra else 0)) * q for r in range(world)]
+    fb0, _ = alg_bytes(dict(wl, S=max(per_gpu)))
+    config = {"workload": workload, "desc": wl["desc"], "S_global": S_global, "S_per_gpu": per_gpu, "H": wl["H"],
+              "W": wl["W"], "N": wl["N"], "tile": 16, "pass": "fwd+bwd" if wl["bwd"] else "fwd",
+              "parallelism": (f"batch-sharded x{world} ({scaling} scaling: contiguous scan ranges per GPU, "
+                              "no collective on the data path)"),
+              "l2": l2_policy(fb0)}
+    if q > 1:
+        config["bc_group"] = q
+    return config, S_global, per_gpu
 
 
 def l2_policy(fwd_bytes):

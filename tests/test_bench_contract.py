@@ -54,3 +54,19 @@ def test_bench_reference_arm_two_ranks():  # CPU only: the reference arm never t
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["cores"] >= 1
+    # the config dict is the one the ours arm prints (the driver compares them)
+    sys.path.insert(0, REPO)
+    import bench
+
+    assert d["config"] == bench.build_config("cfg1", 2, "weak")[0]
+
+
+def test_bench_config_shared_by_both_arms():
+    sys.path.insert(0, REPO)
+    import bench
+
+    for wl in bench.WORKLOADS:
+        for world in (1, 2, 8):
+            cfg, S_global, per_gpu = bench.build_config(wl, world, bench.SCALING[wl])
+            assert sum(per_gpu) == S_global and cfg["S_per_gpu"] == per_gpu
+            assert cfg["workload"] == wl and "l2" in cfg
