@@ -164,7 +164,8 @@ int scan2d_backward_band(const scan2d_desc* desc, const void* x, const void* z, 
  *   seq        value the flags carry for this call (must change from call to
  *              call on a link, e.g. a counter; flags start at any other value)
  * strips = scan2d_band_strips(desc).  A producer that never arrives makes the
- * waiting strips give up after 10 s (wrong results instead of a hung GPU).
+ * waiting kernel trap after 10 s (the launch fails instead of hanging the GPU
+ * or continuing on a stale carry).
  * Not for CUDA graph capture (seq is a launch argument). */
 int scan2d_band_strips(const scan2d_desc* desc);
 int scan2d_forward_band_linked(const scan2d_desc* desc, const void* x, const void* z, const void* B,

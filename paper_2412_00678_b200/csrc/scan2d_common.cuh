@@ -219,14 +219,15 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 // Wait (lane 0 polls, the warp follows) until *flag == seq.  A producer that
-// never arrives (a misconfigured link) must not hang the GPU: after 10 s the
-// wait gives up and the strip proceeds with whatever the carry buffer holds.
+// never arrives (a misconfigured link) must neither hang the GPU nor let the
+// strip continue on a stale carry: after 10 s the kernel traps, so the launch
+// fails loudly (cudaErrorLaunchFailure on the next synchronisation).
 __device__ __forceinline__ void link_wait(const int* flag, int seq, int lane) {
   if (lane == 0) {
     const unsigned long long t0 = global_ns();
     while (ld_acquire_sys(flag) != seq) {
       __nanosleep(200);
-      if (global_ns() - t0 > 10000000000ull) break;
+      if (global_ns() - t0 > 10000000000ull) __trap();
     }
   }
   __syncwarp();
