@@ -29,10 +29,10 @@
 // The tile kernels emit the CarryState themselves.  A forward with
 // save_residuals also keeps the GPU residual (checkpoints + strip carries) and
 // the device copies of its inputs in a small per-thread table keyed by the
-// SavedForward's buffers and a fingerprint of its contents; with
-// SCAN2D_SHIM_REUSE=1 the backward reuses them when the SavedForward it is given
-// still matches, by default it uploads the saved inputs and recomputes the
-// residual (always correct).
+// SavedForward's buffers and a fingerprint of its contents; the backward
+// reuses them when the SavedForward it is given still matches (otherwise -- a
+// copy, or edited inputs -- it uploads the saved inputs and recomputes the
+// residual).
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -101,9 +101,11 @@ struct Ctx {
     dev.clear();
     if (st) cudaStreamDestroy(st);
   }
+  // the role's buffer, grown to at least `bytes`; bytes == 0 fetches the existing
+  // buffer unchanged (growing it would drop its contents)
   void* buf(const std::string& role, size_t bytes) {
     DevBuf& b = dev[role];
-    b.grow(bytes ? bytes : 16);
+    if (bytes > 0 || b.p == nullptr) b.grow(bytes > 0 ? bytes : 16);
     return b.p;
   }
   // pinned staging for one call: reserve all bytes first (reset), then carve
@@ -410,12 +412,12 @@ GradBundle<T> tiled_scan_2d_backward(const SavedForward<T>& saved, const Grid<T>
   // the forward's device residual, if this SavedForward is the one it made
   SavedTable& tab = saved_table();
   int slot = -1;
-  // Reusing the forward's device residual is opt-in (SCAN2D_SHIM_REUSE=1): the
-  // reference suites showed one gradcheck case (test_backward.cpp:48-54, T = 1,
-  // after the preceding suites) with wrong gradients on the reuse path that no
-  // isolated replay reproduces; recomputing the residual from the saved inputs
-  // is the validated default (it costs one forward launch per backward).
-  static const bool no_reuse = std::getenv("SCAN2D_SHIM_REUSE") == nullptr;
+  // The forward's device residual and inputs are reused when this SavedForward
+  // is the one it made (SCAN2D_SHIM_REUSE=0 always uploads and recomputes).
+  static const bool no_reuse = [] {
+    const char* v = std::getenv("SCAN2D_SHIM_REUSE");
+    return v != nullptr && v[0] == '0';
+  }();
   for (int k = 0; k < kSavedSlots && !no_reuse; ++k) {
     const SavedEntry& e = tab.e[k];
     if (e.key_x == x.data.data() && e.key_b == saved.inputs.b.data.data() && e.h == h && e.w == w && e.n == n &&
@@ -439,6 +441,37 @@ GradBundle<T> tiled_scan_2d_backward(const SavedForward<T>& saved, const Grid<T>
     tag = tab.e[slot].tag;
     tab.e[slot].last_use = ++tab.clock;
     res = cx.buf(tag + "res", scan2d_residual_bytes(&d));
+    if (std::getenv("SCAN2D_SHIM_DEBUG")) {  // diagnostics: is the slot still what the forward left?
+      cuda_check(cudaStreamSynchronize(cx.st), "debug");
+      auto same = [&](const char* role, const void* host, size_t bytes) {
+        std::vector<unsigned char> dev(bytes);
+        cuda_check(cudaMemcpy(dev.data(), cx.buf(tag + role, 0), bytes, cudaMemcpyDeviceToHost), "debug");
+        const bool eq = std::memcmp(dev.data(), host, bytes) == 0;
+        if (!eq) std::fprintf(stderr, "shim debug: slot %d %s differs from the saved input\n", slot, role);
+      };
+      same("x", x.data.data(), hw);
+      same("z", saved.inputs.z_raw.data.data(), hw);
+      same("b", saved.inputs.b.data.data(), sizeof(T) * saved.inputs.b.data.size());
+      same("c", saved.inputs.c.data.data(), sizeof(T) * saved.inputs.c.data.size());
+      same("a", saved.params.a.data(), sizeof(T) * n);
+      same("d", &saved.params.d_skip, sizeof(T));
+      same("bias", &saved.params.bias, sizeof(T));
+      // recompute the residual and compare
+      const size_t rb = scan2d_residual_bytes(&d), wsf = scan2d_workspace_bytes(&d, SCAN2D_OP_FWD);
+      void* r2 = cx.buf("dbg_res", rb);
+      status_check(scan2d_forward(&d, cx.buf(tag + "x", 0), cx.buf(tag + "z", 0), cx.buf(tag + "b", 0),
+                                  cx.buf(tag + "c", 0), cx.buf(tag + "a", 0), cx.buf(tag + "d", 0),
+                                  cx.buf(tag + "bias", 0), cx.buf("dbg_y", hw), nullptr, nullptr, r2,
+                                  cx.buf("wsf", wsf), wsf, cx.st),
+                   "debug recompute");
+      cuda_check(cudaStreamSynchronize(cx.st), "debug");
+      std::vector<unsigned char> a1(rb), a2(rb);
+      cuda_check(cudaMemcpy(a1.data(), res, rb, cudaMemcpyDeviceToHost), "debug");
+      cuda_check(cudaMemcpy(a2.data(), r2, rb, cudaMemcpyDeviceToHost), "debug");
+      size_t diff = 0;
+      for (size_t i = 0; i < rb; ++i) diff += a1[i] != a2[i];
+      std::fprintf(stderr, "shim debug: slot %d residual %zu bytes, %zu differ from a recompute\n", slot, rb, diff);
+    }
   } else {  // a copied / edited SavedForward: upload its inputs and recompute the residual
     tag = "b_";
     DevScan<T> up(cx, tag, x, saved.inputs, saved.params);
