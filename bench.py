@@ -325,6 +325,10 @@ def main():
                          "by libscan2d_engine_cuda.so over all host cores (lib/bench_shim)")
     ap.add_argument("--compare", action="store_true",
                     help="Table 3: tiled vs naive-2D vs flat-1D operators at 14^2/56^2/200^2, D=1 N=16")
+    ap.add_argument("--bc-reduce", choices=["red", "fixed"], default="red",
+                    help="shared-B/C workloads (G > 1): dB / dC group sums by in-kernel L2 reductions "
+                         "(SCAN2D_FLAG_GROUP_RED; summation order not fixed) or per-scan gradients + a "
+                         "fixed-order reduction kernel (bit-reproducible)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="weak: global batch = N x the workload's; strong: the workload's batch split over N "
                          "GPUs (default per workload, see SCALING)")
@@ -338,7 +342,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     scaling = args.scaling or SCALING[args.workload]
-    config, S_global, per_gpu = build_config(args.workload, world, scaling)
+    config, S_global, per_gpu = build_config(args.workload, world, scaling, args.bc_reduce)
 
     if args.rowband and args.impl == "ours":
         return rowband_main(args, wl, rank, world, local, config)
@@ -372,7 +376,8 @@ def main():
 
     dtype = torch.float32
     sharded = ShardedScan2d(S_global, wl["H"], wl["W"], wl["N"], rank, world, dist=dist,
-                            bc_group=wl.get("G", 1), tile=16, dtype=dtype, device=dev, with_backward=wl["bwd"])
+                            bc_group=wl.get("G", 1), tile=16, dtype=dtype, device=dev, with_backward=wl["bwd"],
+                            group_red=args.bc_reduce == "red")
     shard = sharded.shard
     wl_local = dict(wl, S=shard.count)  # this rank's contiguous scan range of the global batch
     assert [sh.count for sh in sharded.shards] == per_gpu
@@ -466,7 +471,8 @@ def main():
     # the reference fp32 engine's) on the same inputs, for its cost
     if not args.no_accurate:
         aop = Scan2dOp(shard.count, wl["H"], wl["W"], wl["N"], tile=16, dtype=dtype, device=dev,
-                       with_backward=wl["bwd"], accurate=True, bc_group=wl.get("G", 1))
+                       with_backward=wl["bwd"], accurate=True, bc_group=wl.get("G", 1),
+                       group_red=args.bc_reduce == "red")
         aop.check = False
         for _ in range(3):
             aop.forward(*ins, save=wl["bwd"])
@@ -654,7 +660,7 @@ def shim_main(args):
     return 0
 
 
-def build_config(workload, world, scaling):
+def build_config(workload, world, scaling, bc_reduce="red"):
     """The `config` dict of a bench line -- computed from the workload alone, so
     both arms (ours and `--impl reference`) print the identical dict."""
     wl = WORKLOADS[workload]
@@ -674,6 +680,8 @@ def build_config(workload, world, scaling):
               "l2": l2_policy(fb0)}
     if q > 1:
         config["bc_group"] = q
+        config["bc_reduce"] = ("in-kernel L2 reductions (SCAN2D_FLAG_GROUP_RED)" if bc_reduce == "red" else
+                               "per-scan dB/dC + fixed-order reduction kernel")
     return config, S_global, per_gpu
 
 

@@ -83,7 +83,7 @@ typedef struct scan2d_desc {
   int32_t params_period;/* P >= 1, divides S                                    */
   int32_t bc_group;     /* G >= 1, divides S                                    */
   int32_t dtype;        /* SCAN2D_F32 or SCAN2D_F64                            */
-  int32_t flags;        /* 0, or SCAN2D_FLAG_ACCURATE                          */
+  int32_t flags;        /* 0, or SCAN2D_FLAG_ACCURATE | SCAN2D_FLAG_GROUP_RED  */
 } scan2d_desc;
 
 /* desc->flags: fp32 exponentials by range reduction + polynomial (< 1 ulp)
@@ -92,6 +92,15 @@ typedef struct scan2d_desc {
  * N = 1 kernels; other N already use a compensated exponential), at a cost in
  * speed.  No effect on fp64. */
 #define SCAN2D_FLAG_ACCURATE 1
+
+/* desc->flags, backward with bc_group G > 1: dB / dC are summed over the
+ * group in place by L2 reductions (red.global.add) from inside the scan kernel,
+ * instead of per-scan gradients in the workspace plus a fixed-order reduction
+ * kernel.  Faster (no 2 S H W N workspace traffic) but the summation order is
+ * not fixed: results vary in the last bits from run to run, and fp32 denormal
+ * addends flush to zero.  Tile kernels only (N in {4, 8, 16, 32}); other
+ * shapes ignore the flag.  Default off (deterministic). */
+#define SCAN2D_FLAG_GROUP_RED 2
 
 /* Validates a descriptor (the checks of require_shapes, engine.cpp:21-30). */
 int scan2d_check_desc(const scan2d_desc* desc);

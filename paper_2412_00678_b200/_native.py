@@ -135,12 +135,14 @@ def status_string(status: int) -> str:
 
 
 FLAG_ACCURATE = 1  # include/scan2d_cuda.h SCAN2D_FLAG_ACCURATE
+FLAG_GROUP_RED = 2  # include/scan2d_cuda.h SCAN2D_FLAG_GROUP_RED
 
 
-def make_desc(S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=F32, accurate=False) -> Scan2dDesc:
+def make_desc(S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=F32, accurate=False,
+              group_red=False) -> Scan2dDesc:
     return Scan2dDesc(int(S), int(H), int(W), int(N), int(tile),
                       int(S if params_period is None else params_period), int(bc_group), int(dtype),
-                      FLAG_ACCURATE if accurate else 0)
+                      (FLAG_ACCURATE if accurate else 0) | (FLAG_GROUP_RED if group_red else 0))
 
 
 def plan_info(desc: Scan2dDesc, op: int = OP_FWD) -> dict:

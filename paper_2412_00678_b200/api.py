@@ -254,14 +254,14 @@ class Scan2dOp:
     enqueues exactly the library's kernels (no allocator traffic)."""
 
     def __init__(self, S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=torch.float32,
-                 device="cuda", with_backward=True, accurate=False):
+                 device="cuda", with_backward=True, accurate=False, group_red=False):
         self.dev = torch.device(device)
         if self.dev.type == "cuda" and self.dev.index is None:
             self.dev = torch.device("cuda", torch.cuda.current_device())
         self.dtype = dtype
         code = nat.F64 if dtype == torch.float64 else nat.F32
         self.desc = nat.make_desc(S, H, W, N, tile=tile, params_period=params_period, bc_group=bc_group,
-                                  dtype=code, accurate=accurate)
+                                  dtype=code, accurate=accurate, group_red=group_red)
         rc = nat.lib.scan2d_check_desc(C.byref(self.desc))
         if rc != nat.OK:
             raise ValueError(nat.status_string(rc))

@@ -57,7 +57,7 @@ int check_desc(const scan2d_desc* d) {
   if (d->params_period < 1 || d->num_scans % d->params_period != 0) return SCAN2D_EINVAL;
   if (d->bc_group < 1 || d->num_scans % d->bc_group != 0) return SCAN2D_EINVAL;
   if (d->dtype != SCAN2D_F32 && d->dtype != SCAN2D_F64) return SCAN2D_EINVAL;
-  if ((d->flags & ~SCAN2D_FLAG_ACCURATE) != 0) return SCAN2D_EINVAL;
+  if ((d->flags & ~(SCAN2D_FLAG_ACCURATE | SCAN2D_FLAG_GROUP_RED)) != 0) return SCAN2D_EINVAL;
   // N > 128 runs as passes over state groups of <= 128 (scan2d_groups.cu)
   return SCAN2D_OK;
 }
@@ -637,12 +637,14 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   // the state-vector outputs take 16-byte stores (tile kernels: dB / dC, warp
   // kernels: the lane's 4 states); with G > 1 they go to the workspace first
   // (every workspace region starts at a multiple of 256 bytes from its base)
-  const bool ovec = d.bc_group > 1 ? ((reinterpret_cast<uintptr_t>(w) & 15) == 0)
-                                   : ((reinterpret_cast<uintptr_t>(dB) & 15) == 0 &&
-                                      (reinterpret_cast<uintptr_t>(dC) & 15) == 0);
+  const bool out_al = (reinterpret_cast<uintptr_t>(dB) & 15) == 0 && (reinterpret_cast<uintptr_t>(dC) & 15) == 0;
+  const bool want_red = d.bc_group > 1 && (d.flags & SCAN2D_FLAG_GROUP_RED) != 0;
+  const bool ovec = d.bc_group > 1 && !want_red ? ((reinterpret_cast<uintptr_t>(w) & 15) == 0) : out_al;
   if (!ovec) bvec = false;  // no tile backward (it stores dB / dC with 8 / 16-byte vectors)
   rc = plan_with_flags(d, p, xvec, bvec, false, ptr_align({x, z, B, C, dy, dx, dz, dB, dC}));
   if (rc != SCAN2D_OK) return rc;
+  // in-place group reductions: tile kernels only (the others keep the workspace path)
+  const bool red = want_red && p.b.tile;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
   const ResLayout R = res_layout(d, p);
@@ -668,12 +670,18 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   T* dB_ps = static_cast<T*>(dB);
   T* dC_ps = static_cast<T*>(dC);
   const size_t hwn = static_cast<size_t>(d.height) * d.width * d.state_dim;
-  if (d.bc_group > 1) {
+  const int64_t groups = d.num_scans / d.bc_group;
+  if (red) {
+    if (cudaMemsetAsync(dB, 0, groups * hwn * sizeof(T), stream) != cudaSuccess ||
+        cudaMemsetAsync(dC, 0, groups * hwn * sizeof(T), stream) != cudaSuccess)
+      return SCAN2D_ECUDA;
+  } else if (d.bc_group > 1) {
     dB_ps = reinterpret_cast<T*>(w + L.dbc);
     dC_ps = dB_ps + static_cast<size_t>(d.num_scans) * hwn;
   }
   a.dB = dB_ps;
   a.dC = dC_ps;
+  a.red = red;
   a.part = reinterpret_cast<T*>(w + L.part);
   a.rcarry = reinterpret_cast<s2d::CarrySlot<T>*>(w + L.rcarry);
   a.hdr = reinterpret_cast<s2d::WsHdr*>(w + L.ticket);
@@ -705,8 +713,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
       return SCAN2D_ECUDA;
     ++launches;
   }
-  if (d.bc_group > 1) {
-    const int64_t groups = d.num_scans / d.bc_group;
+  if (d.bc_group > 1 && !red) {
     if (s2d::launch_reduce_group<T>(dB_ps, groups, d.bc_group, hwn, static_cast<T*>(dB), stream) !=
             cudaSuccess ||
         s2d::launch_reduce_group<T>(dC_ps, groups, d.bc_group, hwn, static_cast<T*>(dC), stream) !=

@@ -672,6 +672,7 @@ struct Args {
   int pdl;               // launch with programmatic stream serialization (after a begin kernel)
   int xvec, bvec, yvec;  // 16-byte copy units legal for x-like / B-like spans; vector y stores
   int ovec;              // backward: dB / dC 16-byte aligned (vector state stores legal)
+  int red;               // backward, G > 1: dB / dC accumulated in place over the group (L2 reductions)
   // shape
   int64_t S;
   int H, W, N, T_tile, P, G;

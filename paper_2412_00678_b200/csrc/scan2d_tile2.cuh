@@ -127,6 +127,25 @@ __device__ __forceinline__ void stg_stream(T* p, const T (&v)[SH]) {
   }
 }
 
+// SH consecutive elements added into global memory (L2 reductions, no return
+// value): the shared-B/C backward's in-place dB / dC group sums.  fp32 vector
+// reductions flush denormal addends to zero.
+template <typename T, int SH>
+__device__ __forceinline__ void red_states(T* p, const T (&v)[SH]) {
+  if constexpr (sizeof(T) == 4 && SH % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < SH; e += 4)
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + e), "f"(v[e]), "f"(v[e + 1]),
+                   "f"(v[e + 2]), "f"(v[e + 3])
+                   : "memory");
+  } else if constexpr (sizeof(T) == 4 && SH == 2) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v[0]), "f"(v[1]) : "memory");
+  } else {
+#pragma unroll
+    for (int e = 0; e < SH; ++e) atomicAdd(p + e, v[e]);
+  }
+}
+
 // V consecutive elements from / to shared memory (V a power of two)
 template <typename T, int V>
 __device__ __forceinline__ void lds_vec(T (&v)[V], const T* p) {
@@ -215,6 +234,15 @@ struct ColVec {
 #pragma unroll
       for (int k = 0; k < UE; ++k) t[k] = v[h * UE + k];
       stg_stream<T, UE>(p + unit(h) * UE, t);
+    }
+  }
+  __device__ __forceinline__ void red(T* p, const T (&v)[SV]) const {
+#pragma unroll
+    for (int h = 0; h < NU; ++h) {
+      T t[UE];
+#pragma unroll
+      for (int k = 0; k < UE; ++k) t[k] = v[h * UE + k];
+      red_states<T, UE>(p + unit(h) * UE, t);
     }
   }
 };
@@ -838,8 +866,10 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const int wb = ge.wreal - 1;
   const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
   CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
-  T* dBg = a.dB + s * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
-  T* dCg = a.dC + s * HW * N + static_cast<size_t>(c0) * N + s2 * SV;
+  // a.red: dB / dC of the scan's B/C group, summed in place by L2 reductions
+  const int64_t sbc = a.red ? s / a.G : s;
+  T* dBg = a.dB + sbc * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
+  T* dCg = a.dC + sbc * HW * N + static_cast<size_t>(c0) * N + s2 * SV;
   T* dxg = a.dx + s * HW + c0;
   T* dzg = a.dz + s * HW + c0;
   const int jg2 = c0 + j2;
@@ -1056,7 +1086,10 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           T dc[SV];
 #pragma unroll
           for (int e = 0; e < SV; ++e) dc[e] = dyv * hcur[e];
-          cv.stg(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
+          if (a.red)
+            cv.red(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
+          else
+            cv.stg(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
         }
       }
       T acc[SV];  // DAs holds the lane's dA partials in natural state order
@@ -1120,7 +1153,12 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           }
           ddp[jj] = dd;
           sgb[jj] = sg;
-          if (row_ok && j < ncols) stg_stream<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
+          if (row_ok && j < ncols) {
+            if (a.red)
+              red_states<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
+            else
+              stg_stream<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
+          }
         }
         // columns gs .. gs+RG-1 are done with B: load the next tile's (one up) in place
         if (t > 0) {

@@ -52,7 +52,9 @@ def test_accurate_flag_rejects_unknown_bits():
     from paper_2412_00678_b200 import _native as nat
 
     d = nat.make_desc(2, 8, 8, 4)
-    d.flags = 2
-    assert nat.lib.scan2d_check_desc(C.byref(d)) == nat.EINVAL
-    d.flags = nat.FLAG_ACCURATE
-    assert nat.lib.scan2d_check_desc(C.byref(d)) == nat.OK
+    for bad in (4, 8, 1 << 20, -1):
+        d.flags = bad
+        assert nat.lib.scan2d_check_desc(C.byref(d)) == nat.EINVAL
+    for ok in (nat.FLAG_ACCURATE, nat.FLAG_GROUP_RED, nat.FLAG_ACCURATE | nat.FLAG_GROUP_RED):
+        d.flags = ok
+        assert nat.lib.scan2d_check_desc(C.byref(d)) == nat.OK

@@ -1,5 +1,5 @@
 """Diagnostics: CUDA-event fwd / bwd times of one workload through Scan2dOp.
-usage: python tools/time_fb.py S H W N [reps] [G]"""
+usage: python tools/time_fb.py S H W N [reps] [G]   (env P = params period, GROUP_RED=1)"""
 import sys, os, statistics
 import torch
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,12 +12,13 @@ G = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(1)
 r = lambda *s: torch.randn(*s, device=dev, generator=g)
-P = S // G if G > 1 else S
+P = int(os.environ.get("P", S // G if G > 1 else S))
 x, z, dy = r(S, H, W), r(S, H, W), r(S, H, W)
 B, C = r(S // G, H, W, N), r(S // G, H, W, N)
 A = -(0.05 + 0.9 * torch.rand(P, N, device=dev, generator=g))
 D, bias = r(P), 0.5 * r(P)
-op = Scan2dOp(S, H, W, N, device=dev, params_period=P, bc_group=G)
+op = Scan2dOp(S, H, W, N, device=dev, params_period=P, bc_group=G,
+              group_red=os.environ.get("GROUP_RED", "0") == "1")
 op.check = False
 ins = (x, z, B, C, A, D, bias)
 for _ in range(3):
