@@ -644,7 +644,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   rc = plan_with_flags(d, p, xvec, bvec, false, ptr_align({x, z, B, C, dy, dx, dz, dB, dC}));
   if (rc != SCAN2D_OK) return rc;
   // in-place group reductions: tile kernels only (the others keep the workspace path)
-  const bool red = want_red && p.b.tile;
+  const bool red = want_red && p.b.tile && p.b.colsw == 16;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
   const ResLayout R = res_layout(d, p);

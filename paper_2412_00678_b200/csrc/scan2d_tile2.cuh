@@ -800,7 +800,9 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 
 // CW = 16: up to 13 warps (128 registers); CW = 32 (fp32, N <= 16): up to 8
 // warps with the register room for 32-column strips (7 strips cover 200 columns)
-template <typename T, int N, int CW, int SH, bool ACC = false>
+// RED: dB / dC summed over the B/C group in place (a.red; a compile-time
+// variant -- a runtime branch around the stores cost the default kernel 16 %)
+template <typename T, int N, int CW, int SH, bool ACC = false, bool RED = false>
 __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) scan2d_bwd_tile2_kernel(const Args<T> a) {
   using F = Fn<T, ACC>;
   using TS = T2Shape<T, N, CW, SH>;
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
   CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
   // a.red: dB / dC of the scan's B/C group, summed in place by L2 reductions
-  const int64_t sbc = a.red ? s / a.G : s;
+  const int64_t sbc = RED ? s / a.G : s;
   T* dBg = a.dB + sbc * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
   T* dCg = a.dC + sbc * HW * N + static_cast<size_t>(c0) * N + s2 * SV;
   T* dxg = a.dx + s * HW + c0;
@@ -1086,7 +1088,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           T dc[SV];
 #pragma unroll
           for (int e = 0; e < SV; ++e) dc[e] = dyv * hcur[e];
-          if (a.red)
+          if constexpr (RED)
             cv.red(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
           else
             cv.stg(dCg + (static_cast<size_t>(r0 + r) * W + j2) * N, dc);
@@ -1154,7 +1156,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           ddp[jj] = dd;
           sgb[jj] = sg;
           if (row_ok && j < ncols) {
-            if (a.red)
+            if constexpr (RED)
               red_states<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
             else
               stg_stream<T, SH>(dBrow + static_cast<size_t>(j) * N, dBv);
