@@ -160,6 +160,21 @@ struct Fn<float, true> {
 
 // ------------------------------------------------------------ shared memory
 
+// Parameter row p = s mod P and B/C group s / G of scan s, without a 64-bit
+// integer division in the common cases (per-scan parameters P == S, G == 1,
+// or S < 2^31: a 32-bit division) -- the 64-bit ones are software routines
+// that were a visible share of the short row kernels' instructions.
+__device__ __forceinline__ int param_row(int64_t s, int64_t S, int P) {
+  if (P == S) return static_cast<int>(s);
+  if (s < 0x7fffffff) return static_cast<int>(static_cast<uint32_t>(s) % static_cast<uint32_t>(P));
+  return static_cast<int>(s % P);
+}
+__device__ __forceinline__ int64_t bc_row(int64_t s, int G) {
+  if (G == 1) return s;
+  if (s < 0x7fffffff) return static_cast<int64_t>(static_cast<uint32_t>(s) / static_cast<uint32_t>(G));
+  return s / G;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

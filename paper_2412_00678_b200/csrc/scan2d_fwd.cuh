@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
   const LaneMap lm = lane_map<LPC, J>(ge, unit, lane, a.S, W);
   const int q = lm.q, cis = lm.cis, segw = lm.segw, lane_in_seg = lm.lane_in_seg;
   const int64_t sc = lm.scan_ok ? lm.s : 0;
-  const int p = static_cast<int>(sc % a.P);
+  const int p = param_row(sc, a.S, a.P);
   const size_t HW = static_cast<size_t>(H) * W;
   const int nvalid = N - q * SPL;  // valid states of this lane's group (may be <= 0)
 
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(32, 16) scan2d_fwd_kernel(const Args<T> a) {
   stg.x0 = a.x + lm.s0 * HW;
   stg.z0 = a.z + lm.s0 * HW;
   stg.dy0 = nullptr;
-  stg.B0 = a.B + (lm.s0 / a.G) * HW * N;
-  stg.C0 = a.C + (lm.s0 / a.G) * HW * N;
+  stg.B0 = a.B + bc_row(lm.s0, a.G) * HW * N;
+  stg.C0 = a.C + bc_row(lm.s0, a.G) * HW * N;
   stg.xstride = W;
   stg.bstride = static_cast<size_t>(W) * N;
   stg.build(reinterpret_cast<CopyEntry*>(smem + ge.table_off), lane, lm.seg_scans, lm.c0, lm.ncols, N, Np,

@@ -99,13 +99,13 @@ __global__ void __launch_bounds__(128) scan2d_fwd_rows1_kernel(const Args<T> a) 
   const int q = id.q;
   const int64_t s = id.s < a.S ? id.s : a.S - 1;
   const bool ok = id.ok;
-  const int p = static_cast<int>(s % a.P);
+  const int p = param_row(s, a.S, a.P);
   const T A1 = F::a_scale(a.A[p]), Dsk = a.Dskip[p], bias = a.bias[p];
   const size_t HW = static_cast<size_t>(H) * W;
   const T* xg = a.x + s * HW + q * J;
   const T* zg = a.z + s * HW + q * J;
-  const T* Bg = a.B + (s / a.G) * HW + q * J;
-  const T* Cg = a.C + (s / a.G) * HW + q * J;
+  const T* Bg = a.B + bc_row(s, a.G) * HW + q * J;
+  const T* Cg = a.C + bc_row(s, a.G) * HW + q * J;
   T* yg = a.y + s * HW + q * J;
   T* ck = a.ckpt == nullptr ? nullptr : a.ckpt + static_cast<size_t>(s) * (a.plan.nb - 1) * W + q * J;
   T h[J];
@@ -219,15 +219,15 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
   const int q = id.q;
   const int64_t s = id.s < a.S ? id.s : a.S - 1;
   const bool ok = id.ok;
-  const int p = static_cast<int>(s % a.P);
+  const int p = param_row(s, a.S, a.P);
   const T A1 = F::a_scale(a.A[p]), Dsk = a.Dskip[p], bias = a.bias[p];
   const T Au = a.A[p];  // A itself (A1 = A log2 e feeds ex2)
   const size_t HW = static_cast<size_t>(H) * W;
   const size_t off = s * HW + q * J;
   const T* xg = a.x + off;
   const T* zg = a.z + off;
-  const T* Bg = a.B + (s / a.G) * HW + q * J;
-  const T* Cg = a.C + (s / a.G) * HW + q * J;
+  const T* Bg = a.B + bc_row(s, a.G) * HW + q * J;
+  const T* Cg = a.C + bc_row(s, a.G) * HW + q * J;
   const T* yg = a.dy + off;
   T* dxg = a.dx + off;
   T* dzg = a.dz + off;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
     const bool rev = loc >= K;
     const int row = band * K + (rev ? 2 * K - 1 - loc : loc);
     const bool rv = ok && band >= 0 && row >= 0 && row < H;
-    const size_t o = static_cast<size_t>(rv ? row : 0) * W;
+    const int o = rv ? row * W : 0;
     T(*sl)[32][J] = my[jj % NJ];
     cp_lane<T, J>(smem_u32(sl[0][lane]), xg + o, rv);
     cp_lane<T, J>(smem_u32(sl[1][lane]), zg + o, rv);
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
     for (int k = 0; k < J; ++k) hp0[k] = T(0);
     if (ok) {
       if (b > 0)
-        ldg_states<T, J>(hp0, ck + static_cast<size_t>(b - 1) * W);
+        ldg_states<T, J>(hp0, ck + (b - 1) * W);
       else if (a.vtop != nullptr)
         ldg_states<T, J>(hp0, a.vtop + s * W + q * J);
     }
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(128, 4) scan2d_bwd_rows1_kernel(const Args<T> 
         }
       }
       if (ok && i < H) {
-        const size_t o = static_cast<size_t>(i) * W;
+        const int o = i * W;
         stg_row<T, J>(dxg + o, dx);
         stg_row<T, J>(dzg + o, dz);
         stg_row<T, J>(dBg + o, dB);

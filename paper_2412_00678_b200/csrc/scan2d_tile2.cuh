@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   const int wpos = id.strip;
   const int c0 = wpos * CW;
   const int ncols = min(CW, W - c0);
-  const int p = static_cast<int>(s % a.P);
+  const int p = param_row(s, a.S, a.P);
   const size_t HW = static_cast<size_t>(H) * W;
   const size_t WN = static_cast<size_t>(W) * N;
   const T Dsk = a.Dskip[p], bias = a.bias[p];
@@ -580,8 +580,8 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
 
   const T* xg = a.x + s * HW + c0;
   const T* zg = a.z + s * HW + c0;
-  const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
-  const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
+  const T* Bg = a.B + bc_row(s, a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
+  const T* Cg = a.C + bc_row(s, a.G) * HW * N + static_cast<size_t>(c0) * N;
   const uint32_t sbase = smem_u32(sm);
   const bool xrow16 = a.xvec != 0;  // x / z rows 16-byte aligned
 
@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const int wpos = id.strip;
   const int c0 = wpos * CW;
   const int ncols = min(CW, W - c0);
-  const int p = static_cast<int>(s % a.P);
+  const int p = param_row(s, a.S, a.P);
   const size_t HW = static_cast<size_t>(H) * W;
   const size_t WN = static_cast<size_t>(W) * N;
   const T Dsk = a.Dskip[p], bias = a.bias[p];
@@ -852,8 +852,8 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const T* xg = a.x + s * HW + c0;
   const T* zg = a.z + s * HW + c0;
   const T* yg = a.dy + s * HW + c0;
-  const T* Bg = a.B + (s / a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
-  const T* Cg = a.C + (s / a.G) * HW * N + static_cast<size_t>(c0) * N;
+  const T* Bg = a.B + bc_row(s, a.G) * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
+  const T* Cg = a.C + bc_row(s, a.G) * HW * N + static_cast<size_t>(c0) * N;
   const uint32_t sbase = smem_u32(sm);
   const bool xrow16 = a.xvec != 0;  // x / z / dy rows 16-byte aligned
 
@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   const CarrySlot<T>* rc_in = has_succ ? a.rcarry + ((s * wb + wpos) * H) * N + q1 * SH : nullptr;
   CarrySlot<T>* rc_out = has_pred ? a.rcarry + ((s * wb + (wpos - 1)) * H) * N + q1 * SH : nullptr;
   // a.red: dB / dC of the scan's B/C group, summed in place by L2 reductions
-  const int64_t sbc = RED ? s / a.G : s;
+  const int64_t sbc = RED ? bc_row(s, a.G) : s;
   T* dBg = a.dB + sbc * HW * N + static_cast<size_t>(c0) * N + q1 * SH;
   T* dCg = a.dC + sbc * HW * N + static_cast<size_t>(c0) * N + s2 * SV;
   T* dxg = a.dx + s * HW + c0;
