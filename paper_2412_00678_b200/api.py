@@ -123,7 +123,8 @@ def _normalise(x, z, B, C_, A, Dskip, bias):
     return x, z, B, C_, A, Dskip, bias
 
 
-def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int, accurate: bool = False) -> nat.Scan2dDesc:
+def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int, accurate: bool = False,
+                  group_red: bool = False) -> nat.Scan2dDesc:
     """require_shapes (engine.cpp:21-30) + TileConfig (types.hpp:133-146) checks."""
     _check(x.dim() == 3, "scan input must be [S,H,W] (single channel per scan)")
     S, H, W = x.shape
@@ -146,7 +147,7 @@ def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int, accurate: bool = False
         _check(t.device == x.device, "scan2d: all tensors must be on one device")
     G = S // B.shape[0]
     desc = nat.make_desc(S, H, W, N, tile=tile, params_period=P, bc_group=G, dtype=_dtype_code(x),
-                         accurate=accurate)
+                         accurate=accurate, group_red=group_red)
     rc = nat.lib.scan2d_check_desc(C.byref(desc))
     if rc == nat.EINVAL:
         raise ValueError(nat.status_string(rc))
@@ -157,15 +158,18 @@ def make_desc_for(x, z, B, C_, A, Dskip, bias, tile: int, accurate: bool = False
 
 def tiled_scan_2d_forward(x, z, B, C_, A, Dskip, bias, tile: int = 16, threads: int = 1,
                           save_residuals: bool = True, carries: bool = False,
-                          counter=None, accurate: bool = False) -> TiledForwardResult:
+                          counter=None, accurate: bool = False, group_red: bool = False) -> TiledForwardResult:
     """Batched ``tiled_scan_2d_forward`` (engine.hpp:88-94) on the GPU.
+
+    ``accurate``: SCAN2D_FLAG_ACCURATE; ``group_red``: SCAN2D_FLAG_GROUP_RED
+    for the backward of shared-B/C layouts (kept in ``saved``'s descriptor).
 
     ``counter`` (a dict) is filled with the reference element-transfer model
     (engine.cpp:222-229 == memsim.cpp:38-71) when given."""
     del threads  # results are thread-invariant by construction (SPEC.md:302-303)
     x, z, B, C_, A, Dskip, bias = _normalise(x, z, B, C_, A, Dskip, bias)
     x, z, B, C_, A, Dskip, bias = [t.contiguous() for t in (x, z, B, C_, A, Dskip, bias)]
-    desc = make_desc_for(x, z, B, C_, A, Dskip, bias, tile, accurate)
+    desc = make_desc_for(x, z, B, C_, A, Dskip, bias, tile, accurate, group_red)
     S, H, W = x.shape
     N = B.shape[3]
     dev = x.device
@@ -251,7 +255,11 @@ def _charge_counter(counter: dict, S, H, W, N, t):
 class Scan2dOp:
     """Preallocated forward+backward for a fixed descriptor: keeps the
     workspaces, residual and output buffers across calls so a training loop
-    enqueues exactly the library's kernels (no allocator traffic)."""
+    enqueues exactly the library's kernels (no allocator traffic).
+
+    ``accurate`` sets SCAN2D_FLAG_ACCURATE (fp32 exponentials by polynomial);
+    ``group_red`` sets SCAN2D_FLAG_GROUP_RED (bc_group > 1: dB / dC summed in
+    place by L2 reductions -- faster, summation order not fixed)."""
 
     def __init__(self, S, H, W, N, tile=16, params_period=None, bc_group=1, dtype=torch.float32,
                  device="cuda", with_backward=True, accurate=False, group_red=False):

@@ -27,6 +27,20 @@ for (S, H, W, N) in [(2, 9, 40, 16), (3, 9, 212, 16), (2, 6, 40, 4), (2, 5, 20, 
         tiled_scan_2d_backward(res.saved, dy)
         torch.cuda.synchronize()
         print("ok", S, H, W, N, dt, "accurate" if acc else "", flush=True)
+# shared B/C (G > 1) with the in-kernel group reductions and shared parameters (P < S)
+for (S, H, W, N, P, G) in [(4, 9, 40, 16, 2, 4), (6, 9, 212, 16, 3, 3), (4, 6, 20, 4, 4, 2)]:
+    for red in (False, True):
+        g = torch.Generator(device=dev).manual_seed(4)
+        r = lambda *s: torch.randn(*s, generator=g, device=dev)
+        x, z, dy = r(S, H, W), r(S, H, W), r(S, H, W)
+        B, C_ = r(S // G, H, W, N), r(S // G, H, W, N)
+        A = -(0.05 + 0.9 * torch.rand(P, N, generator=g, device=dev))
+        D, bias = r(P), torch.rand(P, generator=g, device=dev) - 0.5
+        op = Scan2dOp(S, H, W, N, params_period=P, bc_group=G, device=dev, group_red=red)
+        op.forward(x, z, B, C_, A, D, bias)
+        op.backward(x, z, B, C_, A, D, bias, dy)
+        torch.cuda.synchronize()
+        print("ok shared", S, H, W, N, P, G, "group_red" if red else "", flush=True)
 # comparators (naive 2D, flat 1D block scan)
 import ctypes as C  # noqa: E402
 

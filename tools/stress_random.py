@@ -61,7 +61,7 @@ def main():
     fails, t0 = 0, time.time()
     todo = [(k, c) for k, c in enumerate(cases(n, seed)) if only is None or k in only]
     for k, (S, H, W, N, P, G, dt, T) in [kc for kc in todo for _ in range(reps)]:
-        label = f"#{k} S={S} {H}x{W} N={N} P={P} G={G} {dt} T={T}"
+        label = f"#{k} S={S} {H}x{W} N={N} P={P} G={G} {dt} T={T}" + (" red" if G > 1 and k % 2 == 0 else "")
         try:
             b = make_batch(orc, S, H, W, N, seed0=9000 + 31 * k, dtype=dt, P=P, G=G)
             (x, z, B, C, A, D, bias), dy = batch_to_torch(b, device="cuda")
@@ -73,7 +73,8 @@ def main():
                     return v
                 x, z, B, C, dy = [shift(t) for t in (x, z, B, C, dy)]
             emit = k % 5 == 0 or os.environ.get("STRESS_EMIT_ALL") == "1"
-            res = tiled_scan_2d_forward(x, z, B, C, A, D, bias, tile=T, carries=emit)
+            red = G > 1 and k % 2 == 0  # in-kernel dB / dC group reductions on half the shared-B/C cases
+            res = tiled_scan_2d_forward(x, z, B, C, A, D, bias, tile=T, carries=emit, group_red=red)
             g = tiled_scan_2d_backward(res.saved, dy)
             torch.cuda.synchronize()
             yg, gg = (1e-12, 1e-10) if dt == "f64" else (1e-4, 1e-4)
