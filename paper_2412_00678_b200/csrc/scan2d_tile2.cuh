@@ -405,15 +405,34 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// shared-window addresses (uint32) versions: the ring computes them with
+// integer arithmetic instead of a generic->shared conversion per call
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar) : "memory");
+}
+#ifndef S2D_MBAR_HINT
+#define S2D_MBAR_HINT 0
+#endif
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+#if S2D_MBAR_HINT > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra W%=;\n\t}" ::"r"(bar),
+      "r"(parity), "n"(S2D_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "W%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W%=;\n\t}" ::"r"(smem_u32(bar)),
+      "@!p bra W%=;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
+#endif
 }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_s(smem_u32(bar), parity); }
 
 // ---- TMA staging of a tile (cp.async.bulk, SASS UBLKCP): lane 0 arms the
 // stage's mbarrier with the tile's byte count and issues one bulk copy per row
@@ -464,6 +483,7 @@ struct CarryRing {
   T* data;
   uint64_t* full;
   uint64_t* empty;
+  uint32_t full_s, empty_s;  // shared-window addresses of full / empty
   static __host__ __device__ size_t bytes(int nw) {
     const size_t nb = nw > 1 ? nw - 1 : 0;
     return nb * kRing * 32 * SH * sizeof(T) + 2 * nb * kRing * sizeof(uint64_t);
@@ -473,23 +493,27 @@ struct CarryRing {
     data = reinterpret_cast<T*>(base);
     full = reinterpret_cast<uint64_t*>(base + static_cast<size_t>(nb) * kRing * 32 * SH * sizeof(T));
     empty = full + nb * kRing;
+    full_s = smem_u32(full);
+    empty_s = smem_u32(empty);
   }
   // producer side: tile index u (0, 1, 2, ... in the warp's own visiting order)
   __device__ __forceinline__ void put(int b, int u, int lane, const T (&v)[SH]) {
     const int k = u % kRing;
-    mbar_wait(empty + b * kRing + k, ((u / kRing) & 1) ^ 1);
-    T* d = data + ((static_cast<size_t>(b) * kRing + k) * 32 + lane) * SH;
+    const uint32_t bo = static_cast<uint32_t>(b * kRing + k) * 8u;
+    mbar_wait_s(empty_s + bo, ((u / kRing) & 1) ^ 1);
+    T* d = data + ((b * kRing + k) * 32 + lane) * SH;
 #pragma unroll
     for (int e = 0; e < SH; ++e) d[e] = v[e];
-    mbar_arrive(full + b * kRing + k);
+    mbar_arrive_s(full_s + bo);
   }
   __device__ __forceinline__ void get(int b, int u, int lane, T (&v)[SH]) {
     const int k = u % kRing;
-    mbar_wait(full + b * kRing + k, (u / kRing) & 1);
-    const T* d = data + ((static_cast<size_t>(b) * kRing + k) * 32 + lane) * SH;
+    const uint32_t bo = static_cast<uint32_t>(b * kRing + k) * 8u;
+    mbar_wait_s(full_s + bo, (u / kRing) & 1);
+    const T* d = data + ((b * kRing + k) * 32 + lane) * SH;
 #pragma unroll
     for (int e = 0; e < SH; ++e) v[e] = d[e];
-    mbar_arrive(empty + b * kRing + k);
+    mbar_arrive_s(empty_s + bo);
   }
 };
 
