@@ -186,6 +186,8 @@ int make_plan(const scan2d_desc& d, Plan& p) {
                d.height <= env_int("SCAN2D_PF_ALL_ROWS", 32);
   }
   if (rows1_shape(d)) {
+    // row forward: 1 = line prefetches pfd rows ahead, 2 = bulk spans (SCAN2D_ROWS1_PFMODE)
+    p.pf_mode = env_int("SCAN2D_ROWS1_PFMODE", 1);
     p.K = 4;
     p.nb = static_cast<int>(ceil_div(d.height, p.K));
     p.Q = d.width;

@@ -42,6 +42,15 @@ __device__ __forceinline__ void stg_row(T* p, const T (&v)[J]) {
   stg_stream<T, J>(p, v);
 }
 
+// Bulk L2 prefetch (TMA unit, SASS UBLKPF) of rows [r0, r1) of one scan's map:
+// one contiguous span, widened to 16-byte boundaries.
+template <typename T>
+__device__ __forceinline__ void bulk_rows_l2(const T* map, int r0, int r1, int W) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(map + static_cast<size_t>(r0) * W) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(map + static_cast<size_t>(r1) * W) + 15) & ~uintptr_t(15);
+  if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), static_cast<uint32_t>(a1 - a0));
+}
+
 // inclusive segmented scan of affine pairs (a, b): element q composed after q-1
 template <typename T, int SEG>
 __device__ __forceinline__ void seg_scan_fwd(T& ap, T& b, int q) {
@@ -154,8 +163,19 @@ __global__ void __launch_bounds__(128) scan2d_fwd_rows1_kernel(const Args<T> a) 
           if (ck != nullptr && r == K - 1 && i < H - 1) stg_row<T, J>(ck + static_cast<size_t>(i / K) * W, h);
           if (a.vbot != nullptr && i == H - 1) stg_row<T, J>(a.vbot + s * W + q * J, h);
         }
-        // L2 prefetch of row i + 2K, then refill this slot with row i + K
-        if (ok && i + a.plan.pfd < H) {
+        // L2 prefetch: bulk spans of 2K rows, 2K..4K rows ahead (K..4K at the
+        // start), by each scan's first lane (pf_mode 2); or row i + pfd line by line.  Then refill this
+        // slot with row i + K.
+        if (a.plan.pf_mode == 2) {
+          if (r == 0 && (i0 % (2 * K)) == 0 && q == 0 && ok && i0 + K < H) {
+            const int p0 = i0 == 0 ? K : i0 + 2 * K, p1 = min(H, i0 + 4 * K);
+            const T* xm = xg - q * J;
+            bulk_rows_l2(xm, p0, p1, W);
+            bulk_rows_l2(zg - q * J, p0, p1, W);
+            bulk_rows_l2(Bg - q * J, p0, p1, W);
+            bulk_rows_l2(Cg - q * J, p0, p1, W);
+          }
+        } else if (ok && i + a.plan.pfd < H) {
           const size_t o2 = static_cast<size_t>(i + a.plan.pfd) * W;
           prefetch_l2(xg + o2);
           prefetch_l2(zg + o2);
