@@ -21,7 +21,8 @@
  *    workspace and the residual ("saved forward") buffer.
  *  - Stream ordered: work is enqueued on `stream`; nothing synchronises the host.
  *  - Deterministic: identical inputs give identical output bits run to run (no
- *    floating-point atomics; scalar reductions use a fixed order).
+ *    floating-point atomics; scalar reductions use a fixed order) -- except
+ *    dB / dC under SCAN2D_FLAG_GROUP_RED, which the caller opts into.
  *  - Thread safe across distinct (stream, workspace) pairs.
  *  - Workspaces need no initialisation.  Launches whose column strips are
  *    chained across CTAs keep a small header at the start of the workspace (a
@@ -32,6 +33,8 @@
  *    carry region once (stale words can never satisfy a tag).
  *  - Output alignment: none required; 16-byte aligned dB / dC enable the
  *    vector-store kernels (otherwise a scalar-store kernel family runs).
+ *    The workspace and the residual buffer must be 16-byte aligned (any
+ *    cudaMalloc / framework allocation is); otherwise SCAN2D_EINVAL.
  *
  * Layouts (S scans = flattened batch x channel, per-scan reference Grid layout,
  * types.hpp:55-57, N fastest):

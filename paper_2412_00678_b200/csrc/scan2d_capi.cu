@@ -298,6 +298,8 @@ bool rows1_geo(s2d::Geo& g, const scan2d_desc& d, int align_bytes, bool bwd) {
   return true;
 }
 
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 // largest power of two <= 16 dividing every address (x-like and B-like operands)
 int ptr_align(std::initializer_list<const void*> ps) {
   int a = 16;
@@ -571,6 +573,7 @@ int forward_impl(const scan2d_desc& d, const void* x, const void* z, const void*
   if (rc != SCAN2D_OK) return rc;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_FWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
+  if (!al16(ws) || !al16(residual)) return SCAN2D_EINVAL;  // (header, carry slots, vector stores)
   unsigned char* w = static_cast<unsigned char*>(ws);
   Args<T> a{};
   fill_common(a, d, p, x, z, B, C, A, Dskip, bias);
@@ -641,7 +644,11 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   // (every workspace region starts at a multiple of 256 bytes from its base)
   const bool out_al = (reinterpret_cast<uintptr_t>(dB) & 15) == 0 && (reinterpret_cast<uintptr_t>(dC) & 15) == 0;
   const bool want_red = d.bc_group > 1 && (d.flags & SCAN2D_FLAG_GROUP_RED) != 0;
-  const bool ovec = d.bc_group > 1 && !want_red ? ((reinterpret_cast<uintptr_t>(w) & 15) == 0) : out_al;
+  // (G > 1: the per-scan gradients go to the workspace unless the tile kernel
+  // reduces in place -- which kernel runs is known only after planning, so with
+  // the reduction requested both destinations must allow 16-byte stores)
+  const bool ws_al = (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+  const bool ovec = d.bc_group > 1 ? ws_al && (!want_red || out_al) : out_al;
   if (!ovec) bvec = false;  // no tile backward (it stores dB / dC with 8 / 16-byte vectors)
   rc = plan_with_flags(d, p, xvec, bvec, false, ptr_align({x, z, B, C, dy, dx, dz, dB, dC}));
   if (rc != SCAN2D_OK) return rc;
@@ -649,6 +656,7 @@ int backward_impl(const scan2d_desc& d, const void* x, const void* z, const void
   const bool red = want_red && p.b.tile && p.b.colsw == 16;
   const WsLayout L = ws_layout(d, p, SCAN2D_OP_BWD);
   if (ws_bytes < L.total || ws == nullptr) return SCAN2D_ENOMEM;
+  if (!al16(ws) || !al16(residual)) return SCAN2D_EINVAL;  // (header, carry slots, vector stores)
   const ResLayout R = res_layout(d, p);
   const unsigned char* r = static_cast<const unsigned char*>(residual);
   Args<T> a{};

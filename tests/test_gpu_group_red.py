@@ -74,3 +74,40 @@ def test_group_red_model_layout_full_size(orc):
     ref = oracle_bwd(orc, b, "f64")
     for k in ("dB", "dC"):
         assert rel_error(g1[k].reshape(-1), np.asarray(ref[k]).reshape(-1)) <= 1e-4, k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("misalign", ["outputs", "workspace"])
+def test_group_red_unaligned_destinations(orc, misalign):
+    """With the flag set, dB / dC at an odd element offset must not take
+    16-byte vector stores (the planner then runs the scalar-store kernels
+    through the workspace path); a workspace off 16-byte alignment is refused
+    (SCAN2D_EINVAL, include/scan2d_cuda.h) instead of faulting."""
+    import ctypes as C
+
+    from paper_2412_00678_b200 import _native as nat
+    from paper_2412_00678_b200.api import Scan2dOp
+
+    S, H, W, N, G = 6, 20, 40, 16, 3
+    b = make_batch(orc, S, H, W, N, seed0=4300, dtype="f32", P=S, G=G)
+    (x, z, B, C_, A, D, bias), dy = batch_to_torch(b, device="cuda")
+    op = Scan2dOp(S, H, W, N, bc_group=G, device="cuda", group_red=True)
+    op.forward(x, z, B, C_, A, D, bias)
+    shapes = [(S, H, W), (S, H, W), (S, N), (S // G, H, W, N), (S // G, H, W, N), (S,), (S,)]
+    off = 1 if misalign == "outputs" else 0
+    outs = [torch.full((int(np.prod(s)) + off,), float("nan"), device="cuda")[off:].view(s) for s in shapes]
+    wsb = op.wsb_bytes
+    wbuf = torch.empty(wsb + 64, dtype=torch.uint8, device="cuda")
+    ws = wbuf[4:] if misalign == "workspace" else wbuf
+    p = lambda t: C.c_void_p(t.data_ptr())
+    rc = nat.lib.scan2d_backward(C.byref(op.desc), p(x), p(z), p(B), p(C_), p(A), p(D), p(bias), p(op.residual),
+                                 p(dy), *[p(o) for o in outs], p(ws), wsb,
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if misalign == "workspace":  # documented requirement: 16-byte aligned workspace / residual
+        assert rc == nat.EINVAL
+        return
+    assert rc == nat.OK, nat.status_string(rc)
+    torch.cuda.synchronize()
+    ref = oracle_bwd(orc, b, "f64")
+    for k, name in enumerate(NAMES):
+        assert rel_error(outs[k].cpu().numpy().reshape(-1), np.asarray(ref[name]).reshape(-1)) <= 1e-4, name
