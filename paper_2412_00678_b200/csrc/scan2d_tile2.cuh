@@ -395,7 +395,7 @@ constexpr int kRing = 4;  // carry ring depth (tiles)
 // warps (strips) per CTA at most.  Forward: 13 (128 registers, 13 strips = a
 // 200-column scan per CTA).  Backward: 12 = 3 per SM sub-partition, so up to
 // 168 registers per thread (no spills).
-constexpr int kTileMaxWarps = 13;
+constexpr int kTileMaxWarps = 15;
 constexpr int kTileMaxWarpsBwd = 12;
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
