@@ -503,15 +503,13 @@ def main():
     #      reference call's contract -- host data in, host results out -- with the
     #      copies pipelined against the kernels inside the library)
     e2e = None
-    if wl.get("G", 1) > 1:  # scan2d_train_host serves the reference operator contract (per-scan B / C)
-        e2e = {"value": None, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "note": "host-operand path serves per-scan B/C only (scan2d_train_host)"}
-    if not args.no_e2e and e2e is None:
+    if not args.no_e2e:
         from paper_2412_00678_b200.api import train_host
 
         hin = [t.cpu().pin_memory() for t in ins]
         hdy = dy.cpu().pin_memory() if wl["bwd"] else None
-        outs = train_host(*hin, dy=hdy, chunks=args.e2e_chunks)
+        red = wl.get("G", 1) > 1 and args.bc_reduce == "red"
+        outs = train_host(*hin, dy=hdy, chunks=args.e2e_chunks, group_red=red)
         torch.cuda.synchronize()
         h2d = sum(t.numel() * t.element_size() for t in hin) + (hdy.numel() * 4 if wl["bwd"] else 0)
         d2h = sum(t.numel() * t.element_size() for t in outs if t is not None)
@@ -521,7 +519,7 @@ def main():
         torch.cuda.synchronize()
         ea.record(stream)
         for _ in range(k2):
-            train_host(*hin, dy=hdy, outs=outs, chunks=args.e2e_chunks)
+            train_host(*hin, dy=hdy, outs=outs, chunks=args.e2e_chunks, group_red=red)
             stream.synchronize()
         eb.record(stream)
         torch.cuda.synchronize()

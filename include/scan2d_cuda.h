@@ -210,9 +210,11 @@ int scan2d_ipc_close(void* base);
  * cudaStreamSynchronize(stream) before reading the outputs).  Host buffers
  * should be page-locked (cudaHostAlloc / cudaHostRegister) for the copies to
  * run asynchronously.  Device buffers are cached per host thread and
- * descriptor.  Requires per-scan parameters and B/C (P == S, G == 1), else
- * SCAN2D_EUNSUPPORTED.  With dy == NULL only y is written.  chunks <= 0 picks
- * the count automatically (>= 32 MB of input per chunk, at most 8). */
+ * descriptor.  Shared B/C (G > 1) and shared parameters (P < S) are cut at
+ * multiples of lcm(G, P) scans (whole groups and parameter periods; the
+ * parameter gradients are summed over the chunks in chunk order); a single
+ * group / period is one chunk.  With dy == NULL only y is written.  chunks <= 0
+ * picks the count automatically (>= 32 MB of input per chunk, at most 8). */
 int scan2d_train_host(const scan2d_desc* desc, const void* x, const void* z, const void* B,
                       const void* C, const void* A, const void* Dskip, const void* bias,
                       const void* dy, void* y, void* dx, void* dz, void* dA, void* dB, void* dC,

@@ -448,21 +448,24 @@ class Scan2dBandOp:
 
 
 def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 0, tile: int = 16,
-               sync: bool = True):
+               sync: bool = True, group_red: bool = False):
     """One training step with HOST (CPU, ideally pinned) tensors through the C
     ABI's ``scan2d_train_host``: chunked host->device copies, kernels and
     device->host copies overlap on three streams of the current device.
     Returns ``outs`` = (y, dx, dz, dA, dB, dC, dD, dbias) as host tensors
-    (gradients None when ``dy`` is None).  Per-scan parameters and B/C only
-    (A [S,N], Dskip / bias [S]).  With ``sync=False`` the call returns as soon
-    as the work is enqueued and the outputs are valid only after
-    ``torch.cuda.current_stream().synchronize()``."""
+    (gradients None when ``dy`` is None).  B / C may be shared by groups of G
+    scans ([S/G,H,W,N]) and A / Dskip / bias by the period P ([P,N], [P]) --
+    the model layout; chunks are then cut at whole groups / periods.  With
+    ``sync=False`` the call returns as soon as the work is enqueued and the
+    outputs are valid only after ``torch.cuda.current_stream().synchronize()``."""
     _check(x.dim() == 3, "train_host: x must be [S,H,W]")
     S, H, W = x.shape
-    _check(B.dim() == 4, "train_host: B must be [S,H,W,N]")
+    _check(B.dim() == 4 and B.shape[0] >= 1 and S % B.shape[0] == 0, "train_host: B must be [S/G,H,W,N]")
+    _check(A.dim() == 2 and A.shape[0] >= 1 and S % A.shape[0] == 0, "train_host: A must be [P,N], P dividing S")
     N = B.shape[-1]
-    ins = [("x", x, (S, H, W)), ("z", z, (S, H, W)), ("B", B, (S, H, W, N)), ("C", C_, (S, H, W, N)),
-           ("A", A, (S, N)), ("Dskip", Dskip, (S,)), ("bias", bias, (S,))]
+    SB, P = B.shape[0], A.shape[0]
+    ins = [("x", x, (S, H, W)), ("z", z, (S, H, W)), ("B", B, (SB, H, W, N)), ("C", C_, (SB, H, W, N)),
+           ("A", A, (P, N)), ("Dskip", Dskip, (P,)), ("bias", bias, (P,))]
     if dy is not None:
         ins.append(("dy", dy, (S, H, W)))
     _check(x.dtype in (torch.float32, torch.float64), "train_host: dtype must be float32 or float64")
@@ -472,12 +475,13 @@ def train_host(x, z, B, C_, A, Dskip, bias, dy=None, outs=None, chunks: int = 0,
         _check(t.device.type == "cpu", f"train_host: {name} must be a host tensor")
         _check(t.is_contiguous(), f"train_host: {name} must be contiguous")
     code = nat.F64 if x.dtype == torch.float64 else nat.F32
-    desc = nat.make_desc(S, H, W, N, tile=tile, dtype=code)
+    desc = nat.make_desc(S, H, W, N, tile=tile, params_period=P, bc_group=S // SB, dtype=code,
+                         group_red=group_red)
     if outs is None:
         e = lambda *s: torch.empty(s, dtype=x.dtype).pin_memory()
-        outs = (e(S, H, W),) + ((e(S, H, W), e(S, H, W), e(S, N), e(S, H, W, N), e(S, H, W, N), e(S), e(S))
+        outs = (e(S, H, W),) + ((e(S, H, W), e(S, H, W), e(P, N), e(SB, H, W, N), e(SB, H, W, N), e(P), e(P))
                                 if dy is not None else (None,) * 7)
-    oshapes = [(S, H, W), (S, H, W), (S, H, W), (S, N), (S, H, W, N), (S, H, W, N), (S,), (S,)]
+    oshapes = [(S, H, W), (S, H, W), (S, H, W), (P, N), (SB, H, W, N), (SB, H, W, N), (P,), (P,)]
     for k, (t, shp) in enumerate(zip(outs, oshapes)):
         if k > 0 and dy is None:
             continue

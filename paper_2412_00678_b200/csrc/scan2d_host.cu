@@ -8,9 +8,14 @@
 // both directions overlap each other and the kernels.
 //
 // Three device buffer sets rotate, so chunk k+2's host->device copies never
-// wait for chunk k's device->host copies to drain.  The per-scan parameters
-// (A, Dskip, bias) go over once before the first chunk and their gradients come
-// back once after the last, so a chunk costs five copies each way.  The first
+// wait for chunk k's device->host copies to drain.  The parameters (A, Dskip,
+// bias) go over once before the first chunk and their gradients come back once
+// after the last, so a chunk costs five copies each way.  Shared B/C (G > 1)
+// and shared parameters (P < S, the model layout) are served by cutting the
+// scans at multiples of lcm(G, P): a chunk then owns whole B/C groups (its
+// dB / dC slices are its own) and starts at parameter row 0, so it uses the
+// whole parameter table and its parameter gradients are added into the
+// totals on the compute stream, in chunk order (bit-reproducible).  The first
 // and the last base chunk are split into 1/8, 1/8, 1/4, 1/2 pieces (ramp): the
 // device->host direction starts, and the host->device direction finishes, after
 // one small piece instead of one whole chunk.  Device buffers, streams and
@@ -39,6 +44,7 @@ struct Slot {
   void* residual = nullptr;
   void* wsf = nullptr;
   void* wsb = nullptr;
+  void* dpar[3] = {};  // shared parameters (P < S): this chunk's dA, dDskip, dbias
   size_t wsf_bytes = 0, wsb_bytes = 0;
 };
 
@@ -63,6 +69,7 @@ struct Ctx {
       cudaFree(s.residual);
       cudaFree(s.wsf);
       cudaFree(s.wsb);
+      for (void* p : s.dpar) cudaFree(p);
     }
     for (int i = 0; i < kSlots; ++i) {
       cudaEventDestroy(ev_in[i]);
@@ -80,12 +87,39 @@ thread_local std::unique_ptr<Ctx> g_ctx;
 
 bool same(const scan2d_desc& a, const scan2d_desc& b) { return std::memcmp(&a, &b, sizeof(a)) == 0; }
 
-// element counts of the per-chunk operands for s scans (P == S, G == 1)
+template <typename T>
+__global__ void accumulate_kernel(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[t] += src[t];
+}
+
+int accumulate(int dtype, void* dst, const void* src, int64_t n, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 4));
+  if (n <= 0) return SCAN2D_OK;
+  if (dtype == SCAN2D_F64)
+    accumulate_kernel<double><<<blocks, 256, 0, st>>>(static_cast<double*>(dst), static_cast<const double*>(src), n);
+  else
+    accumulate_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(dst), static_cast<const float*>(src), n);
+  return cudaGetLastError() == cudaSuccess ? SCAN2D_OK : SCAN2D_ECUDA;
+}
+
+int64_t gcd64(int64_t a, int64_t b) { return b == 0 ? a : gcd64(b, a % b); }
+
+// scans per chunk quantum: whole B/C groups, and whole parameter periods when
+// the parameters are shared (P < S)
+int64_t quantum(const scan2d_desc& d) {
+  const int64_t G = d.bc_group, P = d.params_period;
+  if (P == d.num_scans) return G;
+  return G / gcd64(G, P) * P;
+}
+
+// element counts of the per-chunk operands for s scans (s a multiple of G)
 void counts(const scan2d_desc& d, int64_t s, size_t (&in)[kIn], size_t (&out)[kOut]) {
   const size_t hw = static_cast<size_t>(d.height) * d.width, n = d.state_dim;
-  const size_t S = static_cast<size_t>(s);
-  const size_t c[kIn] = {S * hw, S * hw, S * hw * n, S * hw * n, S * hw};
-  const size_t o[kOut] = {S * hw, S * hw, S * hw, S * hw * n, S * hw * n};
+  const size_t S = static_cast<size_t>(s), SB = static_cast<size_t>(s / d.bc_group);
+  const size_t c[kIn] = {S * hw, S * hw, SB * hw * n, SB * hw * n, S * hw};
+  const size_t o[kOut] = {S * hw, S * hw, S * hw, SB * hw * n, SB * hw * n};
   for (int i = 0; i < kIn; ++i) in[i] = c[i];
   for (int i = 0; i < kOut; ++i) out[i] = o[i];
 }
@@ -136,7 +170,9 @@ int setup(const scan2d_desc& d, int chunks, bool with_bwd) {
   c->chunks = chunks;
   c->with_bwd = with_bwd;
   c->device = dev;
-  c->chunk_scans = static_cast<int>((d.num_scans + chunks - 1) / chunks);
+  const int64_t q = quantum(d), units = d.num_scans / q;
+  const int64_t cu = (units + chunks - 1) / chunks;  // quanta per base chunk
+  c->chunk_scans = static_cast<int>(cu * q);
   if (cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->comp, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
@@ -147,14 +183,15 @@ int setup(const scan2d_desc& d, int chunks, bool with_bwd) {
         cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming) != cudaSuccess)
       return SCAN2D_ECUDA;
   if (cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess) return SCAN2D_ECUDA;
-  c->sched = schedule(d.num_scans, chunks, c->chunk_scans);
+  c->sched = schedule(units, chunks, cu);  // in quanta
+  for (auto& pc : c->sched) pc.first *= q, pc.second *= q;
+  const bool shared_par = d.params_period != d.num_scans;
   scan2d_desc cd = d;
   cd.num_scans = c->chunk_scans;
-  cd.params_period = c->chunk_scans;
-  cd.bc_group = 1;
+  cd.params_period = shared_par ? d.params_period : c->chunk_scans;
   const size_t es = es_of(d.dtype);
-  const size_t S = static_cast<size_t>(d.num_scans), N = static_cast<size_t>(d.state_dim);
-  const size_t pc[3] = {S * N, S, S};
+  const size_t P = static_cast<size_t>(d.params_period), N = static_cast<size_t>(d.state_dim);
+  const size_t pc[3] = {P * N, P, P};
   for (int i = 0; i < 3; ++i) {
     if (cudaMalloc(&c->par[i], pc[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
     if (with_bwd && cudaMalloc(&c->dpar[i], pc[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
@@ -172,6 +209,9 @@ int setup(const scan2d_desc& d, int chunks, bool with_bwd) {
       s.wsb_bytes = scan2d_workspace_bytes(&cd, SCAN2D_OP_BWD);
       if (cudaMalloc(&s.wsb, s.wsb_bytes) != cudaSuccess) return SCAN2D_ENOMEM;
       if (cudaMalloc(&s.residual, scan2d_residual_bytes(&cd)) != cudaSuccess) return SCAN2D_ENOMEM;
+      if (shared_par)
+        for (int i = 0; i < 3; ++i)
+          if (cudaMalloc(&s.dpar[i], pc[i] * es) != cudaSuccess) return SCAN2D_ENOMEM;
     }
   }
   g_ctx = std::move(c);
@@ -198,16 +238,17 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
     for (int i = 0; i < kIn; ++i) bytes += in[i] * es;
     chunks = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, bytes / (32u << 20))));
   }
-  if (chunks > d.num_scans) chunks = static_cast<int>(d.num_scans);
-  // chunks split scans, so parameters and B/C must be per scan
-  if (d.params_period != d.num_scans || d.bc_group != 1) return SCAN2D_EUNSUPPORTED;
+  // chunks are cut at whole quanta (B/C groups, parameter periods)
+  const int64_t nunits = d.num_scans / quantum(d);
+  if (chunks > nunits) chunks = static_cast<int>(nunits);
   rc = setup(d, chunks, bwd);
   if (rc != SCAN2D_OK) return rc;
   Ctx& c = *g_ctx;
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
   const size_t N = static_cast<size_t>(d.state_dim);
-  const size_t pc[3] = {static_cast<size_t>(d.num_scans) * N, static_cast<size_t>(d.num_scans),
-                        static_cast<size_t>(d.num_scans)};
+  const bool shared_par = d.params_period != d.num_scans;
+  const size_t P = static_cast<size_t>(d.params_period);
+  const size_t pc[3] = {P * N, P, P};
   const void* hpar[3] = {A, Dskip, bias};
   void* hdpar[3] = {dA, dDskip, dbias};
   const void* hin[kIn] = {x, z, B, C, dy};
@@ -218,6 +259,11 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
   for (int i = 0; i < 3; ++i)
     if (cudaMemcpyAsync(c.par[i], hpar[i], pc[i] * es, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
       return SCAN2D_ECUDA;
+  if (bwd && shared_par) {  // shared parameter gradients: summed over the chunks in order
+    cudaStreamWaitEvent(c.comp, c.ev_start, 0);
+    for (int i = 0; i < 3; ++i)
+      if (cudaMemsetAsync(c.dpar[i], 0, pc[i] * es, c.comp) != cudaSuccess) return SCAN2D_ECUDA;
+  }
   const int nchunk = static_cast<int>(c.sched.size());
   for (int k = 0; k < nchunk; ++k) {
     const int sl = k % Ctx::kSlots;
@@ -235,19 +281,28 @@ extern "C" int scan2d_train_host(const scan2d_desc* desc, const void* x, const v
     cudaStreamWaitEvent(c.comp, c.ev_in[sl], 0);
     scan2d_desc cd = d;
     cd.num_scans = sk;
-    cd.params_period = static_cast<int32_t>(sk);
-    const char* pA = static_cast<const char*>(c.par[0]) + s0 * N * es;
-    const char* pD = static_cast<const char*>(c.par[1]) + s0 * es;
-    const char* pb = static_cast<const char*>(c.par[2]) + s0 * es;
+    cd.params_period = shared_par ? d.params_period : static_cast<int32_t>(sk);
+    const int64_t p0 = shared_par ? 0 : s0;  // first parameter row of the chunk
+    const char* pA = static_cast<const char*>(c.par[0]) + p0 * N * es;
+    const char* pD = static_cast<const char*>(c.par[1]) + p0 * es;
+    const char* pb = static_cast<const char*>(c.par[2]) + p0 * es;
     rc = scan2d_forward(&cd, s.in[0], s.in[1], s.in[2], s.in[3], pA, pD, pb, s.out[0], nullptr, nullptr,
                         bwd ? s.residual : nullptr, s.wsf, s.wsf_bytes, reinterpret_cast<scan2d_stream_t>(c.comp));
     if (rc != SCAN2D_OK) return rc;
     if (bwd) {
+      void* gA = shared_par ? s.dpar[0] : static_cast<char*>(c.dpar[0]) + s0 * N * es;
+      void* gD = shared_par ? s.dpar[1] : static_cast<char*>(c.dpar[1]) + s0 * es;
+      void* gb = shared_par ? s.dpar[2] : static_cast<char*>(c.dpar[2]) + s0 * es;
       rc = scan2d_backward(&cd, s.in[0], s.in[1], s.in[2], s.in[3], pA, pD, pb, s.residual, s.in[4], s.out[1],
-                           s.out[2], static_cast<char*>(c.dpar[0]) + s0 * N * es, s.out[3], s.out[4],
-                           static_cast<char*>(c.dpar[1]) + s0 * es, static_cast<char*>(c.dpar[2]) + s0 * es,
-                           s.wsb, s.wsb_bytes, reinterpret_cast<scan2d_stream_t>(c.comp));
+                           s.out[2], gA, s.out[3], s.out[4], gD, gb, s.wsb, s.wsb_bytes,
+                           reinterpret_cast<scan2d_stream_t>(c.comp));
       if (rc != SCAN2D_OK) return rc;
+      if (shared_par) {
+        const void* src[3] = {gA, gD, gb};
+        for (int i = 0; i < 3; ++i)
+          if ((rc = accumulate(d.dtype, c.dpar[i], src[i], static_cast<int64_t>(pc[i]), c.comp)) != SCAN2D_OK)
+            return rc;
+      }
     }
     cudaEventRecord(c.ev_out[sl], c.comp);
     cudaStreamWaitEvent(c.d2h, c.ev_out[sl], 0);

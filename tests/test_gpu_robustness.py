@@ -176,7 +176,7 @@ def test_train_host_rejects_bad_operands(orc):
     b = make_batch(orc, S, H, W, N, seed0=7100, dtype="f32")
     host = [torch.from_numpy(np.ascontiguousarray(v)) for v in (b.x, b.z, b.B, b.C, b.A, b.D, b.bias)]
     bad = list(host)
-    bad[4] = host[4][:1]  # A as [P, N] with P < S: the host path needs per-scan parameters
+    bad[4] = host[4][:, :2].contiguous()  # A with the wrong state dimension
     with pytest.raises(ValueError, match="A"):
         train_host(*bad)
     bad = list(host)
