@@ -392,6 +392,15 @@ __device__ __forceinline__ void prefetch_tile_l2(int mode, int lane, int r0, int
 // words, and CTAs take tickets so a producer CTA is always resident first.
 
 constexpr int kRing = 4;  // carry ring depth (tiles)
+// cross-CTA horizontal carries loaded one tile ahead: forward (measured: cfg2
+// with scans straddling CTAs 176.7 -> 158.2 us, 64 x 1024^2 1918 -> 1809 us)
+// and backward (S2D_CARRY_PF_B)
+#ifndef S2D_CARRY_PF
+#define S2D_CARRY_PF 1
+#endif
+#ifndef S2D_CARRY_PF_B
+#define S2D_CARRY_PF_B 0
+#endif
 // warps (strips) per CTA at most.  Forward: 13 (128 registers, 13 strips = a
 // 200-column scan per CTA).  Backward: 12 = 3 per SM sub-partition, so up to
 // 168 registers per thread (no spills).
@@ -661,6 +670,16 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
   T bc[CW][SH];
   load_b_rows<T, CW, SH>(bc, Bg, r1, H, WN, ncols, N);
 
+  // horizontal carry from a strip in another CTA: loaded one tile ahead (the
+  // tag tells a stale word; the resolve then re-polls)
+  CarryPre<T, SH> cpre;
+#if S2D_CARRY_PF
+  if constexpr (sizeof(T) == 4) {
+    if (has_pred && !pred_ring && r1 < H)
+      carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(r1) * N),
+                     *reinterpret_cast<CarryPre<float, SH>*>(&cpre));
+  }
+#endif
   const int pft = a.plan.pf_all ? 0 : a.plan.pft_f;
   const int pfmode = a.plan.pf_mode;
   if (a.plan.pf_all)
@@ -695,12 +714,13 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
     cp_async_commit();
     const int i1 = r0 + r1;
     const bool row_ok = i1 < H;
-    CarryPre<T, SH> cpre;
+#if !S2D_CARRY_PF
     if constexpr (sizeof(T) == 4) {
       if (has_pred && !pred_ring && row_ok)
         carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
                        *reinterpret_cast<CarryPre<float, SH>*>(&cpre));
     }
+#endif
     cp_async_wait<1>();
     if (tma) mbar_wait(tbar + (t & 1), (t >> 1) & 1);
     __syncwarp();
@@ -734,6 +754,11 @@ __global__ void __launch_bounds__(32 * kTileMaxWarps, 1) scan2d_fwd_tile2_kernel
         carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1) * N),
                           *reinterpret_cast<CarryPre<float, SH>*>(&cpre), row_tag(epoch, i1),
                           *reinterpret_cast<float(*)[SH]>(hh));
+#if S2D_CARRY_PF
+        if (i1 + R < H)
+          carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(hc_in + static_cast<size_t>(i1 + R) * N),
+                         *reinterpret_cast<CarryPre<float, SH>*>(&cpre));
+#endif
       } else {
         carry_get_wait<T, SH>(hc_in + static_cast<size_t>(i1) * N, hh, row_tag(epoch, i1), SH);
       }
@@ -959,6 +984,15 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
   if (a.plan.pf_all)
     for (int t2 = ntiles - 2; t2 >= 0; --t2)
       prefetch_tile_l2<T, R>(pfmode, lane, t2 * R, H, ncols, N, WN, W, Bg - q1 * SH, Cg, xg, zg, yg, xrow16);
+#if S2D_CARRY_PF_B
+  CarryPre<T, SH> rpre;  // reverse carry from a strip in another CTA, one tile ahead
+  if constexpr (sizeof(T) == 4) {
+    const int ib = (ntiles - 1) * R + r1;
+    if (has_succ && !succ_ring && ib < H)
+      carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(ib) * N),
+                     *reinterpret_cast<CarryPre<float, SH>*>(&rpre));
+  }
+#endif
   for (int t = ntiles - 1; t >= 0; --t) {
     const int u = ntiles - 1 - t;  // visiting index (ring phase)
     const int r0 = t * R;
@@ -1000,12 +1034,14 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
 #pragma unroll
     for (int e = 0; e < SH; ++e) hh0[e] = hh0n[e], hh0n[e] = T(0);
     if (has_pred && t > 0) ldg_states<T, SH>(hh0n, hc_in + static_cast<size_t>(i1 - R) * N);
+#if !S2D_CARRY_PF_B
     CarryPre<T, SH> rpre;
     if constexpr (sizeof(T) == 4) {
       if (has_succ && !succ_ring && row_ok)
         carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
                        *reinterpret_cast<CarryPre<float, SH>*>(&rpre));
     }
+#endif
     T hp0[SV];  // h(r0 - 1, j): the forward checkpoint
 #pragma unroll
     for (int e = 0; e < SV; ++e) hp0[e] = T(0);
@@ -1138,11 +1174,16 @@ __global__ void __launch_bounds__(CW == 16 ? 32 * kTileMaxWarpsBwd : 256, 1) sca
           for (int e = 0; e < SH; ++e) rho[e] = T(0);
         }
       } else if (has_succ && row_ok) {
-        if constexpr (sizeof(T) == 4)
+        if constexpr (sizeof(T) == 4) {
           carry_resolve<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1) * N),
                             *reinterpret_cast<CarryPre<float, SH>*>(&rpre), row_tag(epoch, i1),
                             *reinterpret_cast<float(*)[SH]>(rho));
-        else
+#if S2D_CARRY_PF_B
+          if (t > 0)  // the next tile up
+            carry_load<SH>(reinterpret_cast<const CarrySlot<float>*>(rc_in + static_cast<size_t>(i1 - R) * N),
+                           *reinterpret_cast<CarryPre<float, SH>*>(&rpre));
+#endif
+        } else
           carry_get_wait<T, SH>(rc_in + static_cast<size_t>(i1) * N, rho, row_tag(epoch, i1), SH);
       }
       const T* dr = Ds + r1 * CW;
