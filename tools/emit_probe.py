@@ -1,3 +1,6 @@
+"""Diagnostics: CarryState emission (ph / pv) of tiled_scan_2d_forward against
+the fp64 oracle over reference tile sizes T in {1, 2, 3, 6, 16} (GPU).
+usage: python tools/emit_probe.py"""
 import sys, numpy as np, torch
 sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 from oracle_lib import Oracle, rel_error
