@@ -138,3 +138,19 @@ def test_emission_forward_then_backward(orc, S, H, W, N, P, dtype, T):
         torch.cuda.synchronize()
         _check(orc, b, res.y, [g.dx, g.dz_raw, g.da, g.db, g.dc, g.dd, g.dbias], dtype,
                f"emit S={S} {H}x{W} N={N} {dtype} T={T}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("S,H,W,N,label", [
+    (37, 40, 200, 16, "one wave, balanced 4-warp runs: every scan straddles CTAs"),
+    (31, 16, 1024, 16, "two waves of 13-warp CTAs -> one wave of 14-warp CTAs (last-wave fill)"),
+    (150, 8, 56, 8, "one wave, runs over all SMs, 4-strip scans split across CTAs"),
+])
+def test_tile_launch_geometries(orc, S, H, W, N, label):
+    """The launch geometries the planner picks by size (scan2d_kern.inc
+    launch_tile): balanced one-wave launches whose scans straddle CTAs (their
+    carries cross through the tagged global words, loaded a tile ahead) and
+    multi-wave forwards widened to 14 warps -- forward and backward against
+    the fp64 oracle."""
+    b, op, y, grads = _run(orc, S, H, W, N, "f32", 5200 + S)
+    _check(orc, b, y, grads, "f32", label)
